@@ -1,0 +1,125 @@
+/* pdq_b200.h — C ABI of the B200 (sm_100a) pattern-defeating-quicksort sort path.
+ *
+ * This library replaces the reference's sort entry point for flat numeric
+ * keys: pkg/src/pdqsort/driver.py:267-270 (sort), :273-279 (sort_with),
+ * :282-292 (sort_with_config), all of which funnel into _sort_range
+ * (driver.py:167-264) with the built-in ordering `operator.lt`.  The
+ * reference is pure Python and has no FFI; INTEGRATION.md shows the ctypes
+ * binding a maintainer adds to driver.py to route `sort()` here.
+ *
+ * Ordering.  Keys are sorted ascending under '<'.  With a payload, elements
+ * are (key, payload) pairs ordered lexicographically — exactly how the
+ * reference orders the list of (key, payload) tuples it is handed for the KV
+ * config (driver.py:267 on tuples).  Float keys are ordered by the IEEE total
+ * order (-0.0 before +0.0; NaNs with the sign bit set first, others last);
+ * for NaN-free input without mixed signed zeros this is identical to '<'.
+ *
+ * All calls are stream-ordered and asynchronous: pdq_sort() enqueues work on
+ * `stream` and returns.  pdq_sort_finish() synchronises the stream and
+ * returns the device-side status and counters.  No global mutable state: two
+ * sorts may run concurrently on different streams with different workspaces.
+ */
+#ifndef PDQ_B200_H
+#define PDQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Key dtypes.  The reference sorts Python ints/floats; the GPU path covers the
+ * fixed-width numeric types of BASELINE.json plus float64. */
+enum pdq_dtype { PDQ_I32 = 0, PDQ_I64 = 1, PDQ_F32 = 2, PDQ_F64 = 3 };
+
+/* Return codes.  The Python layer maps them onto the reference's exception
+ * types: config -> ValueError (driver.py:65-75), dtype/layout -> TypeError,
+ * CUDA -> RuntimeError. */
+enum pdq_status {
+    PDQ_OK = 0,
+    PDQ_ERR_CONFIG = -1,     /* SortConfig rule violated (driver.py:65-75) */
+    PDQ_ERR_DTYPE = -2,      /* unsupported dtype */
+    PDQ_ERR_ALIGN = -3,      /* keys/payload not 16-byte aligned */
+    PDQ_ERR_WORKSPACE = -4,  /* workspace NULL or smaller than pdq_workspace_bytes() */
+    PDQ_ERR_CUDA = -5,       /* a CUDA runtime call failed; see pdq_last_error() */
+    PDQ_ERR_INTERNAL = -6,   /* device-side capacity/invariant failure (reported by finish) */
+    PDQ_ERR_ARG = -7         /* bad argument (negative n, NULL keys with n > 0, ...) */
+};
+
+/* POD mirror of SortConfig (driver.py:47-78) plus the GPU tunables.
+ * The first nine fields keep the reference's names, defaults and validation;
+ * SURVEY.md §8(b) gives each one's GPU meaning. */
+typedef struct pdq_config {
+    int64_t insertion_threshold;      /* 24: validated only (>= 3)                     driver.py:55 */
+    int64_t ninther_threshold;        /* 128: validated only (>= max(8, ins. thresh.)) driver.py:56 */
+    int64_t partial_insertion_budget; /* 8: validated only (>= 0)                      driver.py:57 */
+    int64_t block_size;               /* 64: validated only (>= 1)                     driver.py:58 */
+    int64_t bad_partition_shift;      /* 3: bad iff min(L,R) < size >> shift           driver.py:59,116-124 */
+    int32_t use_block_partition;      /* no-op: the GPU partition is always branchless driver.py:60 */
+    int32_t use_partition_left;       /* enables the equal-key partition_left split    driver.py:61,222 */
+    int32_t use_break_patterns;       /* perturb child pivot samples after a bad split driver.py:62,239 */
+    int32_t use_partial_insertion;    /* enables the sortedness check (K4) exits       driver.py:63,244 */
+    /* ---- GPU fields ---- */
+    int32_t base_case_size;           /* K7 threshold, 32..4096 (default 4096) */
+    int32_t bad_budget;               /* -1: floor(log2 n) (driver.py:263); >= 0 overrides (0 forces the
+                                         radix fallback on the first big segment: test knob) */
+    int32_t reserved[4];
+} pdq_config;
+
+/* Device counters (the GPU analogue of Metrics, instrumentation.py:20-61). */
+typedef struct pdq_stats {
+    int64_t partition_right_calls;  /* segments partitioned with equals-go-right (K2) */
+    int64_t partition_left_calls;   /* segments split with equals-go-left (K3) */
+    int64_t bad_partitions;         /* driver.py:235-238 analogue */
+    int64_t radix_fallbacks;        /* segments that exhausted the budget (K5) */
+    int64_t base_cases;             /* K7 invocations */
+    int64_t max_depth;              /* deepest segment generation */
+    int64_t tiles;                  /* partition tiles processed */
+    int64_t bytes_algorithmic;      /* SURVEY.md §8(d) byte model over the init + sorter kernels, summed
+                                       over the segments they actually processed */
+    int64_t check_result;           /* K4: bit0 a descent seen, bit1 an ascent seen */
+    int64_t segments;               /* descriptors allocated */
+    int64_t status;                 /* 0 or a negative pdq_status */
+    int64_t bytes_check;            /* bytes the K4 check kernel read */
+    int64_t reserved[4];
+} pdq_stats;
+
+/* Fill `cfg` with the reference defaults (driver.py:55-63) and GPU defaults. */
+void pdq_config_default(pdq_config *cfg);
+
+/* 0 if valid, else PDQ_ERR_CONFIG (same rules as driver.py:65-75). */
+int pdq_config_validate(const pdq_config *cfg);
+
+/* Bytes of device workspace one sort of n elements needs (scratch ping-pong
+ * buffer, segment descriptors, task ring, counters). */
+size_t pdq_workspace_bytes(int dtype, int has_payload, int64_t n);
+
+/* Sort n keys (and the optional uint32 payload) in place on the device.
+ * keys / payload: device pointers, 16-byte aligned (torch/cudaMalloc
+ * allocations are).  workspace: device memory of >= pdq_workspace_bytes().
+ * stream: a cudaStream_t (NULL = legacy default stream).  Asynchronous. */
+int pdq_sort(void *keys, int dtype, uint32_t *payload, int64_t n, const pdq_config *cfg,
+             void *workspace, size_t workspace_bytes, void *stream);
+
+/* pdq_sort() that also records two caller-owned CUDA events (cudaEvent_t, may be NULL) on
+ * `stream` immediately before and after the persistent sorter kernel, so a profiler-free
+ * caller can time the dominant kernel alone (bench.py's roofline figure). */
+int pdq_sort_ex(void *keys, int dtype, uint32_t *payload, int64_t n, const pdq_config *cfg,
+                void *workspace, size_t workspace_bytes, void *stream, void *event_sort_begin,
+                void *event_sort_end);
+
+/* Synchronise `stream`, copy the device counters of the last sort that used
+ * `workspace` into *stats (may be NULL) and return its status. */
+int pdq_sort_finish(void *workspace, pdq_stats *stats, void *stream);
+
+/* Thread-local message for the last error returned on this thread. */
+const char *pdq_last_error(void);
+
+/* Library version string. */
+const char *pdq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDQ_B200_H */

@@ -1,0 +1,143 @@
+"""ctypes binding of the C ABI in include/pdq_b200.h (libpdq_b200.so, built in-tree).
+
+There is no fallback: if the shared library is missing, every sort raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "libpdq_b200.so")
+CSRC = os.path.join(HERE, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+
+PDQ_I32, PDQ_I64, PDQ_F32, PDQ_F64 = 0, 1, 2, 3
+
+STATUS = {
+    0: "PDQ_OK",
+    -1: "PDQ_ERR_CONFIG",
+    -2: "PDQ_ERR_DTYPE",
+    -3: "PDQ_ERR_ALIGN",
+    -4: "PDQ_ERR_WORKSPACE",
+    -5: "PDQ_ERR_CUDA",
+    -6: "PDQ_ERR_INTERNAL",
+    -7: "PDQ_ERR_ARG",
+}
+
+# every symbol include/pdq_b200.h declares
+EXPORTS = (
+    "pdq_config_default",
+    "pdq_config_validate",
+    "pdq_workspace_bytes",
+    "pdq_sort",
+    "pdq_sort_ex",
+    "pdq_sort_finish",
+    "pdq_last_error",
+    "pdq_version",
+)
+
+
+class PdqConfig(ctypes.Structure):
+    """POD mirror of pdq_config (include/pdq_b200.h)."""
+
+    _fields_ = [
+        ("insertion_threshold", ctypes.c_int64),
+        ("ninther_threshold", ctypes.c_int64),
+        ("partial_insertion_budget", ctypes.c_int64),
+        ("block_size", ctypes.c_int64),
+        ("bad_partition_shift", ctypes.c_int64),
+        ("use_block_partition", ctypes.c_int32),
+        ("use_partition_left", ctypes.c_int32),
+        ("use_break_patterns", ctypes.c_int32),
+        ("use_partial_insertion", ctypes.c_int32),
+        ("base_case_size", ctypes.c_int32),
+        ("bad_budget", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 4),
+    ]
+
+
+STAT_FIELDS = (
+    "partition_right_calls",
+    "partition_left_calls",
+    "bad_partitions",
+    "radix_fallbacks",
+    "base_cases",
+    "max_depth",
+    "tiles",
+    "bytes_algorithmic",
+    "check_result",
+    "segments",
+    "status",
+    "bytes_check",
+)
+
+
+class PdqStats(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in STAT_FIELDS] + [("reserved", ctypes.c_int64 * 4)]
+
+    def as_dict(self):
+        return {f: int(getattr(self, f)) for f in STAT_FIELDS}
+
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+_lock = threading.Lock()
+_lib = None
+
+
+def build(verbose: bool = False) -> str:
+    """Compile csrc/ into libpdq_b200.so for sm_100a (nvcc cross-compiles without a GPU)."""
+    nvcc = os.environ.get("NVCC", "nvcc")
+    if not os.path.exists(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
+        nvcc = "/usr/local/cuda/bin/nvcc"
+    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-o", LIB_PATH, os.path.join(CSRC, "pdq_capi.cu")]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+def lib() -> ctypes.CDLL:
+    """Load the in-tree shared library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                    "(there is no CPU fallback)")
+            L = ctypes.CDLL(LIB_PATH)
+            P, I64, I, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+            L.pdq_config_default.argtypes = [ctypes.POINTER(PdqConfig)]
+            L.pdq_config_default.restype = None
+            L.pdq_config_validate.argtypes = [ctypes.POINTER(PdqConfig)]
+            L.pdq_config_validate.restype = I
+            L.pdq_workspace_bytes.argtypes = [I, I, I64]
+            L.pdq_workspace_bytes.restype = SZ
+            L.pdq_sort.argtypes = [P, I, P, I64, ctypes.POINTER(PdqConfig), P, SZ, P]
+            L.pdq_sort.restype = I
+            L.pdq_sort_ex.argtypes = [P, I, P, I64, ctypes.POINTER(PdqConfig), P, SZ, P, P, P]
+            L.pdq_sort_ex.restype = I
+            L.pdq_sort_finish.argtypes = [P, ctypes.POINTER(PdqStats), P]
+            L.pdq_sort_finish.restype = I
+            L.pdq_last_error.argtypes = []
+            L.pdq_last_error.restype = ctypes.c_char_p
+            L.pdq_version.argtypes = []
+            L.pdq_version.restype = ctypes.c_char_p
+            _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().pdq_last_error().decode()

@@ -1,0 +1,353 @@
+"""Host side of the B200 sort path: the reference's entry points, routed to the GPU.
+
+Mirrors /root/reference/pkg/src/pdqsort/driver.py:
+
+* :class:`SortConfig` — same fields, defaults and ``ValueError`` rules as
+  driver.py:47-78, plus GPU tunables (``base_case_size``, ``bad_budget``).
+* :func:`sort` (driver.py:267-270), :func:`sort_with` (:273-279) and
+  :func:`sort_with_config` (:282-292) — same names and positional signatures;
+  additive keyword-only ``values=`` carries a uint32 payload.
+* :func:`is_bad_partition` (driver.py:116-124) — the rule K5 applies on the
+  device, exposed for parity tests.
+
+The sort itself never runs on the CPU: every call goes through the C ABI of
+``libpdq_b200.so`` (include/pdq_b200.h) into the sm_100a kernels, and raises
+if that library or a CUDA device is unavailable.  Containers: CUDA tensors
+are sorted in place on the current stream; host containers (list,
+``array.array``, numpy arrays, CPU tensors, lists of ``(key, payload)``
+tuples) are copied to the device, sorted and written back in place, like the
+reference mutates its ``MutableSequence``.
+"""
+
+from __future__ import annotations
+
+import array
+import ctypes
+import operator
+from dataclasses import dataclass
+from typing import Any, Callable, MutableSequence, Optional
+
+import numpy as np
+
+from . import _lib
+
+Ordering = Callable[[Any, Any], bool]
+
+MIN_BREAK_SIZE = 8  # driver.py:44 (pattern breaking is a sample perturbation on the GPU)
+
+
+@dataclass(frozen=True)
+class SortConfig:
+    """Tunables and feature toggles for the sort (driver.py:47-78).
+
+    The first nine fields are the reference's, with its defaults and its
+    validation.  On the GPU ``insertion_threshold``, ``ninther_threshold``,
+    ``partial_insertion_budget`` and ``block_size`` are validated only (the
+    base case, the pivot sample and the tile have their own sizes),
+    ``use_block_partition`` is a no-op (the partition is always branchless),
+    ``use_partition_left`` gates the equal-key split (K3),
+    ``use_break_patterns`` gates the sample perturbation after a bad
+    partition, and ``use_partial_insertion`` gates the sortedness check (K4).
+    """
+
+    insertion_threshold: int = 24
+    ninther_threshold: int = 128
+    partial_insertion_budget: int = 8
+    block_size: int = 64
+    bad_partition_shift: int = 3
+    use_block_partition: bool = True
+    use_partition_left: bool = True
+    use_break_patterns: bool = True
+    use_partial_insertion: bool = True
+    # ---- GPU fields ----
+    base_case_size: int = 4096
+    bad_budget: int = -1
+
+    def __post_init__(self):
+        # driver.py:65-75, same messages
+        if self.insertion_threshold < 3:
+            raise ValueError("insertion_threshold must be >= 3 (pivot selection needs three candidates)")
+        if self.ninther_threshold < max(8, self.insertion_threshold):
+            raise ValueError("ninther_threshold must be >= max(8, insertion_threshold)")
+        if self.partial_insertion_budget < 0:
+            raise ValueError("partial_insertion_budget must be >= 0")
+        if self.block_size < 1:
+            raise ValueError("block_size must be >= 1")
+        if self.bad_partition_shift < 1:
+            raise ValueError("bad_partition_shift must be >= 1")
+        if self.bad_partition_shift > 62:
+            raise ValueError("bad_partition_shift must be <= 62")
+        if not 1024 <= self.base_case_size <= 4096:
+            raise ValueError("base_case_size must be in [1024, 4096]")
+        if self.bad_budget < -1:
+            raise ValueError("bad_budget must be -1 (log2 n) or >= 0")
+
+    def to_c(self) -> _lib.PdqConfig:
+        c = _lib.PdqConfig()
+        for f in ("insertion_threshold", "ninther_threshold", "partial_insertion_budget", "block_size",
+                  "bad_partition_shift", "base_case_size", "bad_budget"):
+            setattr(c, f, int(getattr(self, f)))
+        for f in ("use_block_partition", "use_partition_left", "use_break_patterns", "use_partial_insertion"):
+            setattr(c, f, 1 if getattr(self, f) else 0)
+        return c
+
+
+DEFAULT_CONFIG = SortConfig()
+
+
+def is_bad_partition(left_size: int, right_size: int, total: int, config: SortConfig = DEFAULT_CONFIG) -> bool:
+    """True iff either side is smaller than total * 2**-bad_partition_shift (driver.py:116-124)."""
+    threshold = total >> config.bad_partition_shift
+    return left_size < threshold or right_size < threshold
+
+
+# ---------------------------------------------------------------------------------------------
+# device entry point
+
+_DTYPE_CODE = None
+
+
+def _dtype_code(tdtype) -> int:
+    global _DTYPE_CODE
+    import torch
+
+    if _DTYPE_CODE is None:
+        _DTYPE_CODE = {torch.int32: _lib.PDQ_I32, torch.int64: _lib.PDQ_I64, torch.float32: _lib.PDQ_F32,
+                       torch.float64: _lib.PDQ_F64}
+    code = _DTYPE_CODE.get(tdtype)
+    if code is None:
+        raise TypeError(f"unsupported key dtype {tdtype}; expected int32, int64, float32 or float64")
+    return code
+
+
+def _raise(rc: int, where: str):
+    msg = f"{where}: {_lib.STATUS.get(rc, rc)}: {_lib.last_error()}"
+    if rc == -1:
+        raise ValueError(msg)
+    if rc in (-2, -3):
+        raise TypeError(msg)
+    raise RuntimeError(msg)
+
+
+class DeviceSorter:
+    """Reusable workspace + stream binding for repeated device sorts of one shape.
+
+    ``run(keys, values)`` enqueues a sort on the current stream and returns
+    immediately; ``finish()`` synchronises and returns the device counters
+    (partition calls, bad partitions, base cases, algorithmic bytes, ...).
+    """
+
+    def __init__(self, n: int, dtype, has_payload: bool, device=None, config: SortConfig = DEFAULT_CONFIG):
+        import torch
+
+        self.n = int(n)
+        self.code = _dtype_code(dtype)
+        self.has_payload = bool(has_payload)
+        self.config = config
+        self._cfg = config.to_c()
+        nbytes = _lib.lib().pdq_workspace_bytes(self.code, int(self.has_payload), self.n)
+        self.workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device or "cuda")
+        self.nbytes = nbytes
+
+    def run(self, keys, values=None, stream=None, events=None):
+        """Enqueue the sort.  ``events=(begin, end)``: torch.cuda.Events (enable_timing)
+        recorded immediately around the persistent sorter kernel."""
+        import torch
+
+        if keys.numel() != self.n or _dtype_code(keys.dtype) != self.code:
+            raise TypeError("keys do not match this DeviceSorter's shape/dtype")
+        if (values is not None) != self.has_payload:
+            raise TypeError("payload presence does not match this DeviceSorter")
+        s = stream if stream is not None else torch.cuda.current_stream(keys.device)
+        ev = (None, None)
+        if events is not None:
+            ev = tuple(ctypes.c_void_p(e.cuda_event) for e in events)
+        rc = _lib.lib().pdq_sort_ex(
+            ctypes.c_void_p(keys.data_ptr()), self.code,
+            ctypes.c_void_p(values.data_ptr() if values is not None else 0), self.n,
+            ctypes.byref(self._cfg), ctypes.c_void_p(self.workspace.data_ptr()), self.nbytes,
+            ctypes.c_void_p(s.cuda_stream), ev[0], ev[1])
+        if rc != 0:
+            _raise(rc, "pdq_sort")
+
+    def finish(self, stream=None) -> dict:
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream(self.workspace.device)
+        st = _lib.PdqStats()
+        rc = _lib.lib().pdq_sort_finish(ctypes.c_void_p(self.workspace.data_ptr()), ctypes.byref(st),
+                                        ctypes.c_void_p(s.cuda_stream))
+        if rc != 0:
+            _raise(rc, "pdq_sort_finish")
+        return st.as_dict()
+
+
+def sort_device(keys, values=None, config: SortConfig = DEFAULT_CONFIG) -> dict:
+    """Sort a 1-D contiguous CUDA tensor in place (with an optional uint32 payload
+    carried along, pairs ordered lexicographically).  Synchronous; returns the
+    device counters."""
+    import torch
+
+    if not isinstance(keys, torch.Tensor) or not keys.is_cuda:
+        raise TypeError("sort_device expects a CUDA tensor")
+    if keys.dim() != 1 or not keys.is_contiguous():
+        raise TypeError("keys must be a 1-D contiguous tensor")
+    if values is not None:
+        if not isinstance(values, torch.Tensor) or values.device != keys.device or values.dim() != 1:
+            raise TypeError("values must be a 1-D tensor on the keys' device")
+        if values.dtype not in (torch.int32, torch.uint32) or not values.is_contiguous():
+            raise TypeError("values must be contiguous uint32 (or int32 bit pattern)")
+        if values.numel() != keys.numel():
+            raise ValueError("values must have the same length as keys")
+    n = keys.numel()
+    with torch.cuda.device(keys.device):
+        # 16-byte alignment is part of the ABI; sort an aligned copy of odd views
+        k_al = keys if keys.data_ptr() % 16 == 0 else keys.clone()
+        v_al = values if values is None or values.data_ptr() % 16 == 0 else values.clone()
+        ds = DeviceSorter(n, keys.dtype, values is not None, keys.device, config)
+        ds.run(k_al, v_al)
+        stats = ds.finish()
+        if k_al is not keys:
+            keys.copy_(k_al)
+        if v_al is not values:
+            values.copy_(v_al)
+    return stats
+
+
+# ---------------------------------------------------------------------------------------------
+# host containers -> device -> back in place
+
+_ARRAY_CODES = {"i": np.int32, "l": np.int64, "q": np.int64, "f": np.float32, "d": np.float64}
+
+
+def _sort_numpy(keys: np.ndarray, values: Optional[np.ndarray], config: SortConfig):
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device: the B200 sort path has no CPU fallback")
+    kt = torch.from_numpy(np.ascontiguousarray(keys))
+    dev = torch.device("cuda")
+    kd = kt.to(dev, non_blocking=False)
+    vd = None
+    if values is not None:
+        vd = torch.from_numpy(np.ascontiguousarray(values).view(np.int32)).to(dev)
+    stats = sort_device(kd, vd, config)
+    keys[...] = kd.cpu().numpy()
+    if values is not None:
+        values[...] = vd.cpu().numpy().view(np.uint32)
+    return stats
+
+
+def _as_payload(values) -> np.ndarray:
+    v = np.asarray(values)
+    if v.dtype != np.uint32:
+        if v.dtype.kind not in "iu" or (v.size and (v.min() < 0 or v.max() > 0xFFFFFFFF)):
+            raise TypeError("payload values must be uint32")
+        v = v.astype(np.uint32)
+    return v
+
+
+def _sort_any(data, config: SortConfig, values=None):
+    import torch
+
+    if isinstance(data, torch.Tensor):
+        if data.is_cuda:
+            return sort_device(data, values, config)
+        arr = data.numpy()
+        varr = None if values is None else values.numpy().view(np.uint32)
+        return _sort_numpy(arr, varr, config)
+    if isinstance(data, np.ndarray):
+        if data.ndim != 1:
+            raise TypeError("only 1-D arrays are supported")
+        if values is None:
+            return _sort_numpy(data, None, config)
+        v = values if isinstance(values, np.ndarray) and values.dtype == np.uint32 else _as_payload(values)
+        stats = _sort_numpy(data, v, config)
+        if v is not values:
+            values[:] = v.tolist() if not isinstance(values, np.ndarray) else v
+        return stats
+    if isinstance(data, array.array):
+        dt = _ARRAY_CODES.get(data.typecode)
+        if dt is None or np.dtype(dt).itemsize != data.itemsize:
+            raise TypeError(f"unsupported array typecode {data.typecode!r}")
+        arr = np.frombuffer(data, dtype=dt) if len(data) else np.empty(0, dt)
+        if values is not None:
+            raise TypeError("values= is supported with numpy arrays and tensors")
+        return _sort_numpy(arr, None, config) if len(data) else None
+    if isinstance(data, MutableSequence):
+        n = len(data)
+        if n == 0:
+            return None
+        first = data[0]
+        if isinstance(first, tuple):
+            # KV drop-in: list of (key, payload) tuples, ordered lexicographically like Python tuples
+            if values is not None:
+                raise TypeError("values= cannot be combined with (key, payload) tuples")
+            if any(type(p) is not tuple or len(p) != 2 for p in data):
+                raise TypeError("tuple elements must all be (int key, uint32 payload) pairs")
+            ks = np.array([p[0] for p in data], dtype=object)
+            vs = np.array([p[1] for p in data], dtype=object)
+            keys = _ints_to_int64(ks)
+            vals = _as_payload(_ints_to_int64(vs))
+            stats = _sort_numpy(keys, vals, config)
+            data[:] = list(zip(keys.tolist(), vals.tolist()))
+            return stats
+        kinds = {type(x) for x in data}
+        if kinds <= {int}:
+            keys = _ints_to_int64(np.array(data, dtype=object))
+        elif kinds <= {float}:
+            keys = np.array(data, dtype=np.float64)
+        elif kinds <= {int, float}:
+            keys = np.array(data, dtype=np.float64)
+            if any(type(x) is int and float(x) != x for x in data):
+                raise TypeError("mixed int/float list with ints not exactly representable as float64")
+        else:
+            raise TypeError(f"unsupported element types {sorted(k.__name__ for k in kinds)}")
+        if values is not None:
+            vals = _as_payload(values)
+            stats = _sort_numpy(keys, vals, config)
+            values[:] = vals.tolist()
+        else:
+            stats = _sort_numpy(keys, None, config)
+        out = keys.tolist()
+        if kinds == {int, float}:
+            # keep each element's original Python type (ints stay ints)
+            pool = {}
+            for x in data:
+                pool.setdefault((float(x), type(x)), []).append(x)
+            out = [(pool[(v, int)].pop() if pool.get((v, int)) else pool[(v, float)].pop()) for v in out]
+        data[:] = out
+        return stats
+    raise TypeError(f"unsupported container {type(data).__name__}")
+
+
+def _ints_to_int64(objs: np.ndarray) -> np.ndarray:
+    try:
+        return objs.astype(np.int64)
+    except OverflowError:
+        raise TypeError("integer keys must fit in int64") from None
+
+
+def sort(data: MutableSequence, config: SortConfig = DEFAULT_CONFIG, *, values=None) -> None:
+    """Sort ``data`` in place, ascending under ``<``. Not stable (driver.py:267-270).
+
+    ``values=`` (keyword-only) is a uint32 payload permuted along with the keys;
+    elements are then ordered as (key, payload) pairs.
+    """
+    _sort_any(data, config, values)
+
+
+def sort_with(data: MutableSequence, lt: Ordering, branch_cheap: bool = False) -> None:
+    """Sort ``data`` in place under ``lt`` (driver.py:273-279).  The device path
+    implements the built-in ordering only: ``lt`` must be ``operator.lt``."""
+    sort_with_config(data, lt, DEFAULT_CONFIG, branch_cheap=branch_cheap)
+
+
+def sort_with_config(data: MutableSequence, lt: Ordering, config: SortConfig,
+                     branch_cheap: Optional[bool] = None) -> None:
+    """Sort ``data`` in place under ``lt`` with explicit tunables (driver.py:282-292)."""
+    if lt is not operator.lt:
+        raise NotImplementedError(
+            "the B200 sort path implements the built-in ordering (operator.lt) only; "
+            "custom Python orderings have no device equivalent and there is no CPU fallback")
+    _sort_any(data, config)

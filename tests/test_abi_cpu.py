@@ -1,0 +1,140 @@
+"""CPU-side checks of the boundary: the C-ABI library loads and exports every
+symbol include/pdq_b200.h declares; host logic mirrors driver.py.  No kernel
+is launched here (no GPU in the build container)."""
+
+import ctypes
+import operator
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2106_05123_b200 import DEFAULT_CONFIG, SortConfig, _lib, is_bad_partition, sort_with_config, workloads
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "pdq_b200.h")).read()
+    return set(re.findall(r"\b(pdq_[a-z_]+)\s*\(", src))
+
+
+def test_header_declares_exactly_the_bound_symbols():
+    assert header_symbols() == set(_lib.EXPORTS)
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.lib()
+    for name in header_symbols():
+        assert hasattr(L, name), name
+    assert b"sm_100a" in L.pdq_version()
+
+
+def test_library_is_sm100a_code():
+    out = os.popen(f"cuobjdump -lelf {_lib.LIB_PATH} 2>/dev/null").read()
+    if not out:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out
+
+
+def test_config_struct_layout_and_defaults():
+    L = _lib.lib()
+    c = _lib.PdqConfig()
+    L.pdq_config_default(ctypes.byref(c))
+    assert (c.insertion_threshold, c.ninther_threshold, c.partial_insertion_budget, c.block_size,
+            c.bad_partition_shift) == (24, 128, 8, 64, 3)  # driver.py:55-59
+    assert c.base_case_size == 4096 and c.bad_budget == -1
+    assert ctypes.sizeof(_lib.PdqConfig) == 5 * 8 + 6 * 4 + 4 * 4
+    mine = DEFAULT_CONFIG.to_c()
+    assert bytes(mine) == bytes(c)
+    assert L.pdq_config_validate(ctypes.byref(c)) == 0
+
+
+@pytest.mark.parametrize("kw", [
+    {"insertion_threshold": 2}, {"ninther_threshold": 7}, {"insertion_threshold": 40, "ninther_threshold": 39},
+    {"block_size": 0}, {"bad_partition_shift": 0}, {"partial_insertion_budget": -1},
+])
+def test_config_validation_matches_reference(kw):
+    # pkg/tests/test_driver.py:51-64 — Python raises ValueError, the C ABI returns PDQ_ERR_CONFIG
+    with pytest.raises(ValueError):
+        SortConfig(**kw)
+    base = {f: getattr(DEFAULT_CONFIG, f) for f in DEFAULT_CONFIG.__dataclass_fields__}
+    c = _lib.PdqConfig()
+    _lib.lib().pdq_config_default(ctypes.byref(c))
+    for k, v in kw.items():
+        setattr(c, k, v)
+    assert _lib.lib().pdq_config_validate(ctypes.byref(c)) == -1
+    assert base
+
+
+def test_abi_argument_errors_without_gpu():
+    L = _lib.lib()
+    c = DEFAULT_CONFIG.to_c()
+    # bad dtype / negative n / misaligned keys are rejected before touching the device
+    assert L.pdq_sort(None, 9, None, 10, ctypes.byref(c), None, 0, None) == -2
+    assert L.pdq_sort(None, 0, None, -1, ctypes.byref(c), None, 0, None) == -7
+    assert L.pdq_sort(ctypes.c_void_p(0x1004), 0, None, 10, ctypes.byref(c), None, 0, None) == -3
+    assert L.pdq_sort(ctypes.c_void_p(0x1000), 0, None, 10, ctypes.byref(c), None, 0, None) == -4
+    assert "workspace" in _lib.last_error()
+
+
+def test_workspace_bytes_monotone_and_covers_scratch():
+    L = _lib.lib()
+    for code, w in ((0, 4), (1, 8), (2, 4), (3, 8)):
+        prev = 0
+        for n in (0, 1, 1000, 1 << 20, 1 << 28):
+            b = L.pdq_workspace_bytes(code, 0, n)
+            assert b >= n * w and b >= prev
+            prev = b
+        assert L.pdq_workspace_bytes(code, 1, 1 << 20) >= L.pdq_workspace_bytes(code, 0, 1 << 20) + 4 * (1 << 20)
+    assert L.pdq_workspace_bytes(7, 0, 10) == 0
+    # 2^28 int32: scratch 1 GiB + small metadata
+    assert L.pdq_workspace_bytes(0, 0, 1 << 28) < (1 << 30) * 1.1
+
+
+def test_is_bad_partition_matches_reference_kats():
+    # pkg/tests/test_driver.py:107-123
+    assert is_bad_partition(7, 56, 64) is True
+    assert is_bad_partition(8, 55, 64) is False
+    assert is_bad_partition(32, 31, 64) is False
+    cfg = SortConfig(bad_partition_shift=1)
+    assert is_bad_partition(31, 32, 64, cfg) is True
+    assert is_bad_partition(32, 32, 65, cfg) is False
+
+
+def test_custom_ordering_is_rejected_not_emulated():
+    with pytest.raises(NotImplementedError):
+        sort_with_config([3, 1, 2], lambda a, b: b < a, DEFAULT_CONFIG)
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError):
+        sort_with_config([3, 1, 2], operator.lt, DEFAULT_CONFIG)
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2106_05123_b200")
+    pat = re.compile(r"(^\s*(from|import)\s+oracle\b)|liboracle|oracle\.py", re.M)
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not pat.search(src), f
+
+
+def test_workload_generators_are_deterministic():
+    a = workloads.c1(1000)
+    b = workloads.c1(1000)
+    assert a.dtype == np.int32 and np.array_equal(a, b)
+    k, v = workloads.c5(4096)
+    assert np.unique(k).size == 4096 and v.dtype == np.uint32
+    assert workloads.c2("organ", 10).tolist() == [0, 1, 2, 3, 4, 4, 3, 2, 1, 0]  # datagen.py:121-123
+    x = workloads.c4("normal", 1 << 16)
+    assert not np.isnan(x).any() and not np.any((x == 0) & np.signbit(x))
+    for k_ in workloads.C3_KS[:4]:
+        assert np.unique(workloads.c3(k_, 1 << 16)).size <= k_
