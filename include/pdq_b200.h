@@ -64,7 +64,8 @@ typedef struct pdq_config {
     int32_t base_case_size;           /* K7 threshold, 32..4096 (default 4096) */
     int32_t bad_budget;               /* -1: floor(log2 n) (driver.py:263); >= 0 overrides (0 forces the
                                          radix fallback on the first big segment: test knob) */
-    int32_t reserved[4];
+    int32_t reserved[4];              /* reserved[0] > 0: profiling knob, stop descending at that
+                                         depth (output NOT sorted); keep 0 */
 } pdq_config;
 
 /* Device counters (the GPU analogue of Metrics, instrumentation.py:20-61). */
@@ -82,7 +83,14 @@ typedef struct pdq_stats {
     int64_t segments;               /* descriptors allocated */
     int64_t status;                 /* 0 or a negative pdq_status */
     int64_t bytes_check;            /* bytes the K4 check kernel read */
-    int64_t reserved[4];
+    int64_t cycles_wait;            /* sorter SM cycles (summed over CTAs) waiting for a task */
+    int64_t cycles_work;            /*   ... processing tasks (includes the two below) */
+    int64_t cycles_base;            /*   ... in K7 base cases */
+    int64_t cycles_spawn;           /*   ... sampling pivots and pushing child tiles */
+    int64_t sched_retire;           /* scheduler-thread cycles retiring tiles (fence + counter) */
+    int64_t sched_claim;            /*   ... claiming ring positions */
+    int64_t sched_fetch;            /*   ... polling the ring, copying descriptors, issuing loads */
+    int64_t sched_idle;             /*   ... sleeping with nothing to do */
 } pdq_stats;
 
 /* Fill `cfg` with the reference defaults (driver.py:55-63) and GPU defaults. */

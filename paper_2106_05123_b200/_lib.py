@@ -74,11 +74,19 @@ STAT_FIELDS = (
     "segments",
     "status",
     "bytes_check",
+    "cycles_wait",
+    "cycles_work",
+    "cycles_base",
+    "cycles_spawn",
+    "sched_retire",
+    "sched_claim",
+    "sched_fetch",
+    "sched_idle",
 )
 
 
 class PdqStats(ctypes.Structure):
-    _fields_ = [(f, ctypes.c_int64) for f in STAT_FIELDS] + [("reserved", ctypes.c_int64 * 4)]
+    _fields_ = [(f, ctypes.c_int64) for f in STAT_FIELDS]
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f in STAT_FIELDS}

@@ -110,7 +110,7 @@ struct LaunchInfo {
 
 template <class U, bool FLOAT, bool KV>
 int smem_bytes() {
-    return (int)(2 * (sizeof(U) * TILE + (KV ? 4 * TILE : 0)));
+    return Bufs<U, KV>::bytes();
 }
 
 template <class U, bool FLOAT, bool KV>
@@ -222,6 +222,7 @@ extern "C" int pdq_sort_ex(void *keys, int dtype, uint32_t *payload, int64_t n, 
     P.use_check = cfg.use_partial_insertion ? 1 : 0;
     P.base_size = cfg.base_case_size;
     P.budget0 = cfg.bad_budget;
+    P.debug_depth = cfg.reserved[0];
 
     const bool kv = payload != nullptr;
     switch (dtype) {
@@ -254,6 +255,14 @@ extern "C" int pdq_sort_finish(void *workspace, pdq_stats *out, void *stream) {
         out->segments = (int64_t)st.seg_alloc;
         out->status = (int64_t)st.status;
         out->bytes_check = (int64_t)st.c_bytes_check;
+        out->cycles_wait = (int64_t)st.c_cyc_wait;
+        out->cycles_work = (int64_t)st.c_cyc_work;
+        out->cycles_base = (int64_t)st.c_cyc_base;
+        out->cycles_spawn = (int64_t)st.c_cyc_spawn;
+        out->sched_retire = (int64_t)st.c_sch_retire;
+        out->sched_claim = (int64_t)st.c_sch_claim;
+        out->sched_fetch = (int64_t)st.c_sch_fetch;
+        out->sched_idle = (int64_t)st.c_sch_idle;
     }
     if (st.status == -8) return set_err(PDQ_ERR_INTERNAL, "device watchdog: the task queue stalled for 10 s%s");
     if (st.status) return set_err(PDQ_ERR_INTERNAL, "device-side failure (descriptor capacity)%s");

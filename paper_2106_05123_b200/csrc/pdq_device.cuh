@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace pdq {
 
 constexpr int THREADS = 256;          // threads per CTA in every kernel
@@ -40,11 +42,12 @@ enum : uint32_t {
     I_LEFT = 1u << 1,     // equals-go-left split (partition_left, partition.py:128-181)
     I_HAS_LB = 1u << 2,   // `lb` is a valid lower bound = the reference's predecessor (driver.py:222)
     I_PERTURB = 1u << 3,  // sample positions perturbed (pattern breaking, driver.py:239-243)
+    I_COUNT_EQ = 1u << 4, // the sample's low end repeats the pivot: count keys equal to it
 };
 
 struct __align__(128) Seg {
     int64_t begin, end;   // [begin, end) in element indices
-    uint64_t pivot;       // ordered pivot key
+    uint64_t pivot;       // pivot key: raw bits for partition segments, ordered image for fills
     uint64_t lb;          // ordered lower bound (predecessor), valid iff I_HAS_LB
     uint32_t pivot_v, lb_v;
     uint32_t ntiles;
@@ -77,6 +80,8 @@ struct __align__(128) State {
     // counters (pdq_stats order)
     unsigned long long c_part_right, c_part_left, c_bad, c_fallback, c_base, c_max_depth, c_tiles,
         c_bytes, c_bytes_check;
+    unsigned long long c_cyc_wait, c_cyc_work, c_cyc_base, c_cyc_spawn;  // SM cycles by phase (thread 0)
+    unsigned long long c_sch_retire, c_sch_claim, c_sch_fetch, c_sch_idle;  // scheduler-thread cycles
 };
 
 struct Params {
@@ -96,6 +101,7 @@ struct Params {
     int use_check;
     int base_size;
     int budget0;
+    int debug_depth;   // > 0: segments at this depth are dropped unsorted (profiling only)
 };
 
 // ---- key traits ----------------------------------------------------------------------

@@ -1,41 +1,86 @@
 // pdq_kernels.cuh — the seven kernels of the B200 pdqsort path.
 //
-//   K1 sample pivot          spawn(): SAMPLES evenly spaced keys, CTA bitonic, median
+//   K1 sample pivot          spawn(): SAMPLES stratified keys, CTA bitonic, median
 //                            (generalises choose_pivot, driver.py:81-113)
 //   K2 partition_right       part_tile(): TMA bulk tile -> classify -> ballot/popc ranks ->
-//                            block scan -> one atomic per side per CTA -> 16 B stores
-//                            (block_partition_right, partition.py:184-301)
+//                            block scan -> one atomic per CTA for both sides -> shared-memory
+//                            compaction -> 16 B stores (block_partition_right, partition.py:184-301)
 //   K3 partition_left        part_tile() in I_LEFT mode (partition.py:128-181, driver.py:222-225)
 //   K4 sortedness check      k_check(): adjacent-compare reduction; k_sort prologue reverses
 //                            non-increasing input (partial_insertion_sort path, driver.py:244-250)
 //   K5 bad-partition budget  finalize_part(): is_bad_partition (driver.py:116-124), budget,
 //                            sample perturbation (break_patterns, driver.py:127-156)
-//   K6 segment queue         k_sort(): persistent CTAs popping tasks from a device ring;
-//                            the last tile of a segment spawns its children (driver.py:198-260)
-//   K7 base case             base_case(): segment <= base_case_size sorted in shared memory
-//                            (insertion_sort / unguarded_insertion_sort, small_sorts.py:16-73)
+//   K6 segment queue         k_sort(): persistent, warp-specialised CTAs.  A scheduler warp claims
+//                            tasks from the device ring, issues the TMA bulk loads into a 2-stage
+//                            mbarrier pipeline and retires finished tiles (fence + counter); eight
+//                            compute warps partition tiles and run finalizations (driver.py:198-260)
+//   K7 base case             base_case(): segment <= base_case_size sorted in shared memory by a
+//                            range-reduced LSD radix sort (insertion_sort / unguarded_insertion_sort,
+//                            small_sorts.py:16-73)
 #pragma once
 
 #include "pdq_device.cuh"
 
 namespace pdq {
 
+constexpr int CHUNK = 8;                // tiles per ring task (one claim + one descriptor read + one retire)
+constexpr int RADIX_BITS = 4;
+constexpr int RADIX_DIGITS = 1 << RADIX_BITS;
+constexpr int CNT_BYTES = RADIX_DIGITS * THREADS * 2;  // u16 counters, digit-major
+
+// compute-warp barrier (named barrier 1): the scheduler warp never joins it
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(THREADS) : "memory"); }
+__device__ __forceinline__ int csync_or(int p) {
+    int r;
+    asm volatile(
+        "{\n .reg .pred a, b;\n setp.ne.s32 a, %1, 0;\n bar.red.or.pred b, 1, %2, a;\n selp.s32 %0, 1, 0, b;\n}\n"
+        : "=r"(r)
+        : "r"(p), "n"(THREADS)
+        : "memory");
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, unsigned phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+
 struct Shared {
-    uint64_t bar;
-    uint64_t task;
-    Seg seg;
-    int wl[WARPS], wv[WARPS], weq[WARPS], wloff[WARPS], wroff[WARPS];
+    uint64_t bar;            // TMA stage barrier
+    uint64_t task;           // current ring task word (0 = exit)
+    Seg seg;                 // its descriptor
+    uint64_t ntask;          // prefetched next task (0 = none / not yet published)
+    Seg nseg;
+    unsigned long long npos; // ring position claimed for the next task
+    int nstate;              // 0 none, 1 claimed (unpublished), 2 ready, 3 exit
+    int stage_tile;          // tile index whose TMA load is in flight in the stage, or -1
+    int stage_next;          // 1 if the in-flight stage load belongs to the prefetched next task
+    int wl[WARPS], weq[WARPS];
     long long L, R, lOff, rOff, fL, fE;
     unsigned long long push_pos;
-    int last, loaded;
     uint32_t new_sid;
-    int reused;
-    uint64_t samp_k[SAMPLES];
-    uint32_t samp_v[SAMPLES];
+    int last;
+    uint64_t red_min[WARPS], red_max[WARPS];
+    unsigned red_a[WARPS], red_b[WARPS];
+    uint32_t scan[WARPS];
     // per-CTA counters, flushed once at exit
     unsigned long long s_part_right, s_part_left, s_bad, s_fallback, s_base, s_tiles, s_bytes;
     long long s_max_depth;
+    unsigned long long s_cyc_wait, s_cyc_work, s_cyc_base, s_cyc_spawn;
+    unsigned long long s_sch_retire, s_sch_claim, s_sch_fetch, s_sch_idle;
 };
+
+// Per-CTA shared state and the dynamic shared buffer are namespace-scope so every helper
+// (inlined or not) addresses them as shared memory (LDS/STS, never generic LD/ST).
+__shared__ Shared g_sh;
+extern __shared__ __align__(128) unsigned char g_dsm[];
 
 __device__ __forceinline__ uint32_t mix32(uint64_t x) {
     x ^= x >> 33;
@@ -46,25 +91,60 @@ __device__ __forceinline__ uint32_t mix32(uint64_t x) {
     return (uint32_t)x;
 }
 
+// Dynamic shared memory: the TMA stage, the compaction buffer kc and the base-case scratch kx
+// (keys, then payloads for KV), then the radix counters.  Every pointer is computed
+// arithmetically from the extern shared symbol so the compiler emits LDS/STS, never generic LD/ST.
+template <class U, bool KV>
+struct Bufs {
+    static constexpr int KEY_BYTES = 3 * TILE * (int)sizeof(U);
+    static constexpr int VAL_BYTES = KV ? 3 * TILE * 4 : 0;
+    __device__ __forceinline__ static U *stage() { return reinterpret_cast<U *>(g_dsm); }
+    __device__ __forceinline__ static U *kc() { return reinterpret_cast<U *>(g_dsm) + TILE; }
+    __device__ __forceinline__ static U *kx() { return reinterpret_cast<U *>(g_dsm) + 2 * TILE; }
+    __device__ __forceinline__ static uint32_t *vstage() { return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES); }
+    __device__ __forceinline__ static uint32_t *vc() { return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES) + TILE; }
+    __device__ __forceinline__ static uint32_t *vx() { return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES) + 2 * TILE; }
+    __device__ __forceinline__ static uint16_t *cnt() { return reinterpret_cast<uint16_t *>(g_dsm + KEY_BYTES + VAL_BYTES); }
+    // pivot samples alias kc (free whenever samples are taken)
+    __device__ __forceinline__ static uint64_t *samp_k() { return reinterpret_cast<uint64_t *>(kc()); }
+    __device__ __forceinline__ static uint32_t *samp_v() {
+        return reinterpret_cast<uint32_t *>(reinterpret_cast<unsigned char *>(kc()) + SAMPLES * 8);
+    }
+    __host__ __device__ static constexpr int bytes() { return KEY_BYTES + VAL_BYTES + CNT_BYTES; }
+};
+
 template <class U, bool FLOAT, bool KV>
 struct Sorter {
     using O = Ord<U, FLOAT>;
+    using B = Bufs<U, KV>;
     static constexpr int VEC = 16 / sizeof(U);
     static constexpr int AL = KV ? 4 : VEC;  // element alignment making both key and payload 16 B aligned
     static constexpr int ELEM_BYTES = sizeof(U) + (KV ? 4 : 0);
+    using SU = typename std::conditional<sizeof(U) == 4, int32_t, int64_t>::type;
+
+    // strict order on raw key bits (+ payload): ints compare signed, floats by total order
+    __device__ __forceinline__ static bool lt_raw(U a, uint32_t va, U b, uint32_t vb) {
+        if (FLOAT) {
+            const U oa = O::to(a), ob = O::to(b);
+            if (KV) return oa < ob || (oa == ob && va < vb);
+            return oa < ob;
+        }
+        if (KV) return (SU)a < (SU)b || (a == b && va < vb);
+        return (SU)a < (SU)b;
+    }
 
     // ---- vectorised contiguous store of `len` elements produced by get(i) -----------
     template <class T, class F>
-    __device__ __forceinline__ static void store_run(T *g, int64_t len, F get) {
+    __device__ __forceinline__ static void store_run(T *g, int len, F get) {
         constexpr int V = 16 / sizeof(T);
         const int tid = threadIdx.x;
-        int64_t mis = ((uintptr_t)g / sizeof(T)) & (V - 1);
-        int64_t h = mis ? V - mis : 0;
+        const int mis = (int)(((uintptr_t)g / sizeof(T)) & (V - 1));
+        int h = mis ? V - mis : 0;
         if (h > len) h = len;
-        for (int64_t i = tid; i < h; i += THREADS) g[i] = get(i);
-        int64_t nb = (len - h) / V;
+        if (tid < h) g[tid] = get(tid);
+        const int nb = (len - h) / V;
         uint4 *gv = reinterpret_cast<uint4 *>(g + h);
-        for (int64_t b = tid; b < nb; b += THREADS) {
+        for (int b = tid; b < nb; b += THREADS) {
             union {
                 T t[V];
                 uint4 u;
@@ -73,38 +153,81 @@ struct Sorter {
             for (int q = 0; q < V; ++q) pk.t[q] = get(h + b * V + q);
             gv[b] = pk.u;
         }
-        for (int64_t i = h + nb * V + tid; i < len; i += THREADS) g[i] = get(i);
+        const int t0 = h + nb * V;
+        if (t0 + tid < len) g[t0 + tid] = get(t0 + tid);
     }
 
-    // ---- CTA bitonic sort in shared memory (mirror variant: every compare-exchange puts
-    // the smaller element at the lower index, so virtual +inf padding never moves and pairs
-    // whose upper index is >= m are skipped). ---------------------------------------------
-    template <class K>
-    __device__ static void bitonic(K *k, uint32_t *v, int m) {
-        int P = 1;
-        while (P < m) P <<= 1;
+    // ---- CTA bitonic sort of a power-of-two array in shared memory (pivot samples) -----
+    __device__ static void bitonic_samples(uint64_t *k, uint32_t *v, int P) {
         const int tid = threadIdx.x;
         for (int kk = 2; kk <= P; kk <<= 1) {
             for (int j = kk >> 1; j > 0; j >>= 1) {
                 const int lj = __ffs(j) - 1;
                 const bool mirror = (j == (kk >> 1));
                 for (int p = tid; p < (P >> 1); p += THREADS) {
-                    int i = ((p >> lj) << (lj + 1)) | (p & (j - 1));
-                    int q = mirror ? (i ^ (kk - 1)) : (i + j);
-                    if (q < m) {
-                        K a = k[i], b = k[q];
-                        uint32_t va = KV ? v[i] : 0, vb = KV ? v[q] : 0;
-                        if (pless<KV>(b, vb, a, va)) {
-                            k[i] = b;
-                            k[q] = a;
-                            if (KV) {
-                                v[i] = vb;
-                                v[q] = va;
-                            }
+                    const int i = ((p >> lj) << (lj + 1)) | (p & (j - 1));
+                    const int q = mirror ? (i ^ (kk - 1)) : (i + j);
+                    const uint64_t a = k[i], b = k[q];
+                    const uint32_t va = KV ? v[i] : 0, vb = KV ? v[q] : 0;
+                    if (pless<KV>(b, vb, a, va)) {
+                        k[i] = b;
+                        k[q] = a;
+                        if (KV) {
+                            v[i] = vb;
+                            v[q] = va;
                         }
                     }
                 }
-                __syncthreads();
+                csync();
+            }
+        }
+    }
+
+    // Warp-level bitonic sort of 32*PL (key, payload) pairs held PL per lane (lane l owns
+    // elements [PL*l, PL*l + PL)); no block barriers.
+    template <int PL>
+    __device__ __forceinline__ static void warp_bitonic(uint64_t (&x)[PL], uint32_t (&y)[PL]) {
+        const int lane = threadIdx.x & 31;
+        constexpr int S = 32 * PL;
+#pragma unroll
+        for (int k = 2; k <= S; k <<= 1) {
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const bool mirror = (j == (k >> 1));
+                if (j < PL && (!mirror || k <= PL)) {
+#pragma unroll
+                    for (int i = 0; i < PL; ++i) {
+                        const int p = mirror ? (i ^ (k - 1)) : (i ^ j);
+                        if (p > i && pless<KV>(x[p], y[p], x[i], y[i])) {
+                            const uint64_t t = x[i];
+                            x[i] = x[p];
+                            x[p] = t;
+                            const uint32_t u = y[i];
+                            y[i] = y[p];
+                            y[p] = u;
+                        }
+                    }
+                } else {
+                    // partner lives in another lane: element e ^ j (or the mirror e ^ (k-1))
+                    const int lmask = mirror ? ((k - 1) / PL) : (j / PL);
+                    const bool lower = mirror ? ((lane & ((k >> 1) / PL)) == 0) : ((lane & (j / PL)) == 0);
+                    uint64_t ox[PL];
+                    uint32_t oy[PL];
+#pragma unroll
+                    for (int i = 0; i < PL; ++i) {
+                        const int src = mirror ? (PL - 1 - i) : i;
+                        ox[i] = __shfl_xor_sync(0xffffffffu, x[src], lmask);
+                        oy[i] = KV ? __shfl_xor_sync(0xffffffffu, y[src], lmask) : 0u;
+                    }
+#pragma unroll
+                    for (int i = 0; i < PL; ++i) {
+                        const bool olt = pless<KV>(ox[i], oy[i], x[i], y[i]);
+                        if (lower == olt) {
+                            x[i] = ox[i];
+                            y[i] = oy[i];
+                        }
+                    }
+                }
             }
         }
     }
@@ -124,49 +247,242 @@ struct Sorter {
         atomicExch(&P.st->done, 1u);
     }
 
-    // ---- K7: base case ------------------------------------------------------------------
-    __device__ static void base_case(const Params &P, Shared &sh, U *sk, uint32_t *sv, bool srcB,
-                                     int64_t b, int m) {
+    // ---- K7: base case, range-reduced LSD radix sort in shared memory ---------------------
+    // One stable 4-bit counting pass (per-thread u16 counters, CUB-style) per 4 bits of
+    // (max - min) over the segment's ordered keys: a 4K-key leaf of a uniform int32 sort
+    // spans ~2^16 values, i.e. 4 passes.  KV segments whose keys repeat get payload passes
+    // first so equal keys end up ordered by payload (the tuple order).
+    template <class T>
+    __device__ __forceinline__ static void ld16(const T *s, int base, T (&x)[ITEMS]) {
+        if constexpr (sizeof(T) == 4) {
+            const uint4 *p = reinterpret_cast<const uint4 *>(s + base);
+#pragma unroll
+            for (int q = 0; q < ITEMS / 4; ++q) {
+                const uint4 y = p[q];
+                x[4 * q] = (T)y.x;
+                x[4 * q + 1] = (T)y.y;
+                x[4 * q + 2] = (T)y.z;
+                x[4 * q + 3] = (T)y.w;
+            }
+        } else {
+            const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(s + base);
+#pragma unroll
+            for (int q = 0; q < ITEMS / 2; ++q) {
+                const ulonglong2 y = p[q];
+                x[2 * q] = (T)y.x;
+                x[2 * q + 1] = (T)y.y;
+            }
+        }
+    }
+
+    // One stable counting pass: thread t owns elements [16t, 16t+16) (blocked, so the
+    // thread-major scan of the digit-major u16 counters is the element order) and the counter
+    // column cnt[d][t], which it post-increments again during the scatter.
+    __device__ __noinline__ static void radix_pass(const U *ks, const uint32_t *vs,
+                                                   U *kd, uint32_t *vd, int m, U mn, int shift, bool on_vals,
+                                                   uint32_t vmn) {
+        Shared &sh = g_sh;
         const int tid = threadIdx.x;
+        uint32_t *cnt32 = reinterpret_cast<uint32_t *>(B::cnt());
+#pragma unroll
+        for (int i = 0; i < CNT_BYTES / 4 / THREADS; ++i) cnt32[i * THREADS + tid] = 0;
+        csync();
+        const int base = tid * ITEMS;
+        U k[ITEMS];
+        uint32_t v[ITEMS];
+        ld16<U>(ks, base, k);
+        if (KV) ld16<uint32_t>(vs, base, v);
+        uint16_t *cnt = B::cnt();
+        const int nvalid = m - base;  // items r < nvalid are real
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+            const uint32_t d = on_vals ? ((v[r] - vmn) >> shift) & (RADIX_DIGITS - 1)
+                                       : (uint32_t)((k[r] - mn) >> shift) & (RADIX_DIGITS - 1);
+            const uint32_t a = d * THREADS + tid;
+            const uint32_t c = cnt[a];
+            if (r < nvalid) cnt[a] = (uint16_t)(c + 1);
+        }
+        csync();
+        // exclusive scan over the digit-major counter array: thread t owns entries [16t, 16t+16)
+        {
+            uint4 *c4 = reinterpret_cast<uint4 *>(B::cnt()) + tid * 2;
+            const uint4 x0 = c4[0], x1 = c4[1];
+            uint32_t w0 = x0.x, w1 = x0.y, w2 = x0.z, w3 = x0.w, w4 = x1.x, w5 = x1.y, w6 = x1.z, w7 = x1.w;
+            uint32_t run = 0;
+#define PDQ_PFX(wq)                                     \
+    {                                                   \
+        const uint32_t lo = wq & 0xFFFF, hi = wq >> 16; \
+        const uint32_t e0 = run, e1 = run + lo;         \
+        run = e1 + hi;                                  \
+        wq = e0 | (e1 << 16);                           \
+    }
+            PDQ_PFX(w0) PDQ_PFX(w1) PDQ_PFX(w2) PDQ_PFX(w3) PDQ_PFX(w4) PDQ_PFX(w5) PDQ_PFX(w6) PDQ_PFX(w7)
+#undef PDQ_PFX
+            const int lane = tid & 31, warp = tid >> 5;
+            uint32_t inc = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane == 31) sh.scan[warp] = inc;
+            csync();
+            uint32_t wpre = 0;
+#pragma unroll
+            for (int q = 0; q < WARPS; ++q) wpre += (q < warp) ? sh.scan[q] : 0u;
+            const uint32_t pre = wpre + inc - run;
+            const uint32_t pre2 = pre | (pre << 16);
+            c4[0] = make_uint4(w0 + pre2, w1 + pre2, w2 + pre2, w3 + pre2);
+            c4[1] = make_uint4(w4 + pre2, w5 + pre2, w6 + pre2, w7 + pre2);
+        }
+        csync();
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+            const uint32_t d = on_vals ? ((v[r] - vmn) >> shift) & (RADIX_DIGITS - 1)
+                                       : (uint32_t)((k[r] - mn) >> shift) & (RADIX_DIGITS - 1);
+            const uint32_t a = d * THREADS + tid;
+            const uint32_t pos = cnt[a];
+            if (r < nvalid) {
+                cnt[a] = (uint16_t)(pos + 1);
+                kd[pos] = k[r];
+                if (KV) vd[pos] = v[r];
+            }
+        }
+        csync();
+    }
+
+    __device__ __forceinline__ static U shfl_xor_u(U x, int o) {
+        if (sizeof(U) == 4) return (U)__shfl_xor_sync(0xffffffffu, (uint32_t)x, o);
+        return (U)__shfl_xor_sync(0xffffffffu, (unsigned long long)x, o);
+    }
+    __device__ __forceinline__ static int clz_u(U x) {
+        if (sizeof(U) == 4) return __clz((uint32_t)x);
+        return __clzll((long long)x);
+    }
+
+    __device__ __noinline__ static void base_case(const Params &P, bool srcB, int64_t b,
+                                                  int m) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        const long long c0 = clock64();
         const U *src = (const U *)(srcB ? P.b_keys : P.a_keys);
         const uint32_t *srcv = srcB ? P.b_vals : P.a_vals;
+        U *bufk[2] = {B::kx(), B::kc()};
+        uint32_t *bufv[2] = {KV ? B::vx() : nullptr, KV ? B::vc() : nullptr};
+        // coalesced load (ordered image), min/max of keys and payload
+        U mn = ~(U)0, mx = 0;
+        uint32_t vmn = 0xFFFFFFFFu, vmx = 0;
+#pragma unroll 4
         for (int i = tid; i < m; i += THREADS) {
-            sk[i] = O::to(ldcg(src + b + i));
-            if (KV) sv[i] = ldcg(srcv + b + i);
+            const U x = O::to(ldcg(src + b + i));
+            bufk[0][i] = x;
+            mn = x < mn ? x : mn;
+            mx = x > mx ? x : mx;
+            if (KV) {
+                const uint32_t v = ldcg(srcv + b + i);
+                bufv[0][i] = v;
+                vmn = v < vmn ? v : vmn;
+                vmx = v > vmx ? v : vmx;
+            }
         }
-        __syncthreads();
-        bitonic<U>(sk, sv, m);
-        U *dk = (U *)P.a_keys + b;
-        store_run<U>(dk, m, [&](int64_t i) { return O::from(sk[i]); });
-        if (KV) store_run<uint32_t>(P.a_vals + b, m, [&](int64_t i) { return sv[i]; });
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const U a = shfl_xor_u(mn, o), c = shfl_xor_u(mx, o);
+            mn = a < mn ? a : mn;
+            mx = c > mx ? c : mx;
+            if (KV) {
+                const uint32_t a2 = __shfl_xor_sync(0xffffffffu, vmn, o), c2 = __shfl_xor_sync(0xffffffffu, vmx, o);
+                vmn = a2 < vmn ? a2 : vmn;
+                vmx = c2 > vmx ? c2 : vmx;
+            }
+        }
+        if (lane == 0) {
+            sh.red_min[warp] = (uint64_t)mn;
+            sh.red_max[warp] = (uint64_t)mx;
+            if (KV) {
+                sh.red_a[warp] = vmn;
+                sh.red_b[warp] = vmx;
+            }
+        }
+        csync();
+        mn = (U)sh.red_min[0];
+        mx = (U)sh.red_max[0];
+        if (KV) {
+            vmn = sh.red_a[0];
+            vmx = sh.red_b[0];
+        }
+#pragma unroll
+        for (int q = 1; q < WARPS; ++q) {
+            const U a = (U)sh.red_min[q], c = (U)sh.red_max[q];
+            mn = a < mn ? a : mn;
+            mx = c > mx ? c : mx;
+            if (KV) {
+                vmn = sh.red_a[q] < vmn ? sh.red_a[q] : vmn;
+                vmx = sh.red_b[q] > vmx ? sh.red_b[q] : vmx;
+            }
+        }
+        const U range = mx - mn;
+        const int kbits = range ? (int)(sizeof(U) * 8) - clz_u(range) : 0;
+        int c = 0;  // index of the buffer holding the current order
+        for (int s = 0; s < kbits; s += RADIX_BITS, c ^= 1)
+            radix_pass(bufk[c], bufv[c], bufk[c ^ 1], bufv[c ^ 1], m, mn, s, false, 0);
+        if (KV && vmx != vmn) {
+            // keys repeat? then order equal keys by payload: payload passes, then key passes again
+            int dup = 0;
+            for (int i = tid; i + 1 < m; i += THREADS) dup |= (bufk[c][i] == bufk[c][i + 1]);
+            if (csync_or(dup)) {
+                const int vbits = 32 - __clz(vmx - vmn);
+                for (int s = 0; s < vbits; s += RADIX_BITS, c ^= 1)
+                    radix_pass(bufk[c], bufv[c], bufk[c ^ 1], bufv[c ^ 1], m, mn, s, true, vmn);
+                for (int s = 0; s < kbits; s += RADIX_BITS, c ^= 1)
+                    radix_pass(bufk[c], bufv[c], bufk[c ^ 1], bufv[c ^ 1], m, mn, s, false, 0);
+            }
+        }
+        csync();
+        const U *fk = bufk[c];
+        store_run<U>((U *)P.a_keys + b, m, [&](int i) { return O::from(fk[i]); });
+        if (KV) {
+            const uint32_t *fv = bufv[c];
+            store_run<uint32_t>(P.a_vals + b, m, [&](int i) { return fv[i]; });
+        }
         __threadfence();
-        __syncthreads();
+        csync();
         if (tid == 0) {
             sh.s_base++;
             sh.s_bytes += 2ull * ELEM_BYTES * m;
             finish_keys(P, m);
+            sh.s_cyc_base += clock64() - c0;
         }
-        __syncthreads();
+        csync();
+    }
+
+    __device__ static void push_tasks(const Params &P, uint32_t type, uint32_t sid, uint32_t ntiles) {
+        Shared &sh = g_sh;
+        const unsigned long long pos = sh.push_pos;
+        const uint64_t mask = (1ull << P.log_q) - 1;
+        for (uint32_t t = threadIdx.x; t < ntiles; t += THREADS)
+            *(volatile uint64_t *)&P.ring[(pos + t) & mask] = task_word(pos + t, P.log_q, type, sid, t);
     }
 
     // ---- write [b, e) of A with the pivot (equal-key runs are bitwise identical under the
     // total order, so a fill is exact).  Returns true if it took the reusable descriptor. ---
-    __device__ static bool fill_final(const Params &P, Shared &sh, int64_t b, int64_t e, uint64_t piv,
+    __device__ static bool fill_final(const Params &P, int64_t b, int64_t e, uint64_t piv,
                                       uint32_t pv, int reuse_sid) {
+        Shared &sh = g_sh;
         const int tid = threadIdx.x;
         const int64_t m = e - b;
         if (m <= 0) return false;
         if (m <= INLINE_FILL) {
             const U raw = O::from((U)piv);
-            store_run<U>((U *)P.a_keys + b, m, [&](int64_t) { return raw; });
-            if (KV) store_run<uint32_t>(P.a_vals + b, m, [&](int64_t) { return pv; });
+            store_run<U>((U *)P.a_keys + b, (int)m, [&](int) { return raw; });
+            if (KV) store_run<uint32_t>(P.a_vals + b, (int)m, [&](int) { return pv; });
             __threadfence();
-            __syncthreads();
+            csync();
             if (tid == 0) {
                 sh.s_bytes += (unsigned long long)ELEM_BYTES * m;
                 finish_keys(P, m);
             }
-            __syncthreads();
+            csync();
             return false;
         }
         const uint32_t ntiles = (uint32_t)((e - 1) / TILE - b / TILE + 1);
@@ -187,14 +503,9 @@ struct Sorter {
                 sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)ntiles);
             }
         }
-        __syncthreads();
-        if (sh.new_sid < P.seg_cap) {
-            const unsigned long long pos = sh.push_pos;
-            const uint64_t mask = (1ull << P.log_q) - 1;
-            for (uint32_t t = tid; t < ntiles; t += THREADS)
-                *(volatile uint64_t *)&P.ring[(pos + t) & mask] = task_word(pos + t, P.log_q, T_FILL, sh.new_sid, t);
-        }
-        __syncthreads();
+        csync();
+        if (sh.new_sid < P.seg_cap) push_tasks(P, T_FILL, sh.new_sid, ntiles);
+        csync();
         return reuse_sid >= 0;
     }
 
@@ -202,13 +513,19 @@ struct Sorter {
     // Creates the child segment [b, e) whose data lives in buffer srcB.  Small children are
     // finished right here (K7); big ones get a sampled pivot and their tiles are pushed.
     // Returns true iff the reusable descriptor `reuse_sid` was consumed.
-    __device__ static bool spawn(const Params &P, Shared &sh, U *sk, uint32_t *sv, int64_t b, int64_t e,
-                                 bool srcB, bool has_lb, uint64_t lb, uint32_t lbv, int budget, int depth,
-                                 bool perturb, int reuse_sid) {
+    __device__ static bool spawn(const Params &P, int64_t b, int64_t e, bool srcB,
+                                 bool has_lb, uint64_t lb, uint32_t lbv, int budget, int depth, bool perturb,
+                                 int reuse_sid) {
+        Shared &sh = g_sh;
         const int tid = threadIdx.x;
         const int64_t m = e - b;
         if (m <= 0) return false;
         if (tid == 0 && depth > sh.s_max_depth) sh.s_max_depth = depth;
+        if (P.debug_depth && depth >= P.debug_depth) {  // profiling knob: stop descending (unsorted!)
+            if (tid == 0) finish_keys(P, (unsigned long long)m);
+            csync();
+            return false;
+        }
         if (m == 1) {
             if (tid == 0) {
                 if (srcB) {
@@ -219,30 +536,63 @@ struct Sorter {
                 }
                 finish_keys(P, 1);
             }
-            __syncthreads();
+            csync();
             return false;
         }
         if (m <= P.base_size) {
-            base_case(P, sh, sk, sv, srcB, b, (int)m);
+            base_case(P, srcB, b, (int)m);
             return false;
         }
-        // K1: SAMPLES keys at stratified positions; perturbed strata after a bad partition.
+        // K1: stratified samples (64, or SAMPLES for segments of 2^20+ keys); perturbed strata
+        // after a bad partition.  The median of the sorted sample is the pivot.
+        const long long c0 = clock64();
         const U *src = (const U *)(srcB ? P.b_keys : P.a_keys);
         const uint32_t *srcv = srcB ? P.b_vals : P.a_vals;
-        for (int i = tid; i < SAMPLES; i += THREADS) {
-            int64_t off;
+        const int ns = m >= (1 << 20) ? SAMPLES : 64;
+        auto sample_at = [&](int i) -> int64_t {
             if (perturb)
-                off = ((int64_t)i * m + (int64_t)(mix32((uint64_t)b * 0x9E3779B97F4A7C15ull ^ (uint64_t)(depth * 977 + i)) %
-                                                 (uint64_t)m)) / SAMPLES;
-            else
-                off = ((int64_t)(2 * i + 1) * m) / (2 * SAMPLES);
-            sh.samp_k[i] = (uint64_t)O::to(ldcg(src + b + off));
-            sh.samp_v[i] = KV ? ldcg(srcv + b + off) : 0;
+                return ((int64_t)i * m +
+                        (int64_t)(mix32((uint64_t)b * 0x9E3779B97F4A7C15ull ^ (uint64_t)(depth * 977 + i)) %
+                                  (uint64_t)m)) /
+                       ns;
+            return ((int64_t)(2 * i + 1) * m) / (2 * ns);
+        };
+        uint64_t piv, lo_sample;
+        uint32_t pv;
+        if (ns == 64) {
+            if (tid < 32) {
+                uint64_t x[2];
+                uint32_t y[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int64_t off = sample_at(2 * tid + q);
+                    x[q] = (uint64_t)O::to(ldcg(src + b + off));
+                    y[q] = KV ? ldcg(srcv + b + off) : 0u;
+                }
+                warp_bitonic<2>(x, y);
+                if (tid == 16) {  // element 32 = lane 16, slot 0
+                    B::samp_k()[0] = x[0];
+                    B::samp_v()[0] = y[0];
+                }
+                if (tid == 0) B::samp_k()[1] = x[0];  // the smallest sample
+            }
+            csync();
+            piv = B::samp_k()[0];
+            pv = B::samp_v()[0];
+            lo_sample = B::samp_k()[1];
+        } else {
+            for (int i = tid; i < SAMPLES; i += THREADS) {
+                const int64_t off = sample_at(i);
+                B::samp_k()[i] = (uint64_t)O::to(ldcg(src + b + off));
+                B::samp_v()[i] = KV ? ldcg(srcv + b + off) : 0;
+            }
+            csync();
+            bitonic_samples(B::samp_k(), B::samp_v(), SAMPLES);
+            piv = B::samp_k()[SAMPLES / 2];
+            pv = B::samp_v()[SAMPLES / 2];
+            lo_sample = B::samp_k()[0];
         }
-        __syncthreads();
-        bitonic<uint64_t>(sh.samp_k, sh.samp_v, SAMPLES);
-        const uint64_t piv = sh.samp_k[SAMPLES / 2];
-        const uint32_t pv = sh.samp_v[SAMPLES / 2];
+        const bool dup_heavy = lo_sample == piv;  // the low end of the sample repeats the pivot
         // driver.py:222: a predecessor not less than the pivot equals it -> partition_left
         const bool left = P.use_left && has_lb && !pless<KV>(lb, lbv, piv, pv);
         const uint32_t ntiles = (uint32_t)((e - 1) / TILE - b / TILE + 1);
@@ -257,13 +607,13 @@ struct Sorter {
                 Seg *s = &P.segs[sid];
                 s->begin = b;
                 s->end = e;
-                s->pivot = piv;
+                s->pivot = (uint64_t)O::from((U)piv);  // raw bits: tiles compare raw keys
                 s->pivot_v = pv;
                 s->lb = lb;
                 s->lb_v = lbv;
                 s->ntiles = ntiles;
                 s->info = (srcB ? I_SRC_B : 0) | (left ? I_LEFT : 0) | (has_lb ? I_HAS_LB : 0) |
-                          (perturb ? I_PERTURB : 0);
+                          (perturb ? I_PERTURB : 0) | (dup_heavy ? I_COUNT_EQ : 0);
                 s->budget = budget > 0 ? budget : 0;
                 s->depth = depth;
                 s->cnt_left = 0;
@@ -271,40 +621,39 @@ struct Sorter {
                 s->cnt_eq = 0;
                 s->tiles_done = 0;
                 __threadfence();
-                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)ntiles);
+                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)((ntiles + CHUNK - 1) / CHUNK));
             }
         }
-        __syncthreads();
-        if (sh.new_sid < P.seg_cap) {
-            const unsigned long long pos = sh.push_pos;
-            const uint64_t mask = (1ull << P.log_q) - 1;
-            const uint32_t sid = sh.new_sid;
-            for (uint32_t t = tid; t < ntiles; t += THREADS)
-                *(volatile uint64_t *)&P.ring[(pos + t) & mask] = task_word(pos + t, P.log_q, T_PART, sid, t);
-        }
-        __syncthreads();
+        csync();
+        if (sh.new_sid < P.seg_cap) push_tasks(P, T_PART, sh.new_sid, (ntiles + CHUNK - 1) / CHUNK);
+        csync();
+        if (tid == 0) sh.s_cyc_spawn += clock64() - c0;
         return reuse_sid >= 0;
     }
 
     // ---- K5 + K6: the last tile of a segment decides its children ----------------------------
-    __device__ __noinline__ static void finalize_part(const Params &P, Shared &sh, U *sk, uint32_t *sv, uint32_t sid) {
+    // `sg` is the parent's descriptor (copied when the task was claimed; immutable while it lived).
+    __device__ __noinline__ static void finalize_part(const Params &P, const Seg &sg,
+                                                      uint32_t sid) {
+        Shared &sh = g_sh;
         const int tid = threadIdx.x;
         if (tid == 0) {
             Seg *gs = &P.segs[sid];
-            sh.fL = (long long)atomicAdd(&gs->cnt_left, 0ull);
-            sh.fE = (long long)atomicAdd(&gs->cnt_eq, 0ull);
+            const unsigned long long c = __ldcg(&gs->cnt_left);
+            sh.fL = sg.end - sg.begin < (1ll << 32) ? (long long)(c & 0xFFFFFFFFull) : (long long)c;
+            sh.fE = (long long)__ldcg(&gs->cnt_eq);
         }
-        __syncthreads();
-        const Seg sg = sh.seg;  // parent fields (immutable while it lived)
+        csync();
         const int64_t b = sg.begin, e = sg.end, m = e - b, L = sh.fL;
         const bool srcB = sg.info & I_SRC_B, dstB = !srcB;
+        const uint64_t piv_ord = (uint64_t)O::to((U)sg.pivot);
         if (!(sg.info & I_LEFT)) {
             if (tid == 0) sh.s_part_right++;
             if (sh.fE == m) {
                 // Every key is bitwise equal to the pivot: whichever buffer A holds (the untouched
                 // source, or this pass's output) already is the final, constant run.
                 if (tid == 0) finish_keys(P, (unsigned long long)m);
-                __syncthreads();
+                csync();
                 return;
             }
             const int64_t R = m - L;
@@ -313,9 +662,9 @@ struct Sorter {
             if (tid == 0 && bad) sh.s_bad++;
             const int nb = sg.budget - (bad ? 1 : 0);
             const bool perturb = bad && P.use_break;
-            bool used = spawn(P, sh, sk, sv, b, b + L, dstB, sg.info & I_HAS_LB, sg.lb, sg.lb_v, nb, sg.depth + 1,
+            bool used = spawn(P, b, b + L, dstB, sg.info & I_HAS_LB, sg.lb, sg.lb_v, nb, sg.depth + 1,
                               perturb, (int)sid);
-            spawn(P, sh, sk, sv, b + L, e, dstB, true, sg.pivot, sg.pivot_v, nb, sg.depth + 1, perturb,
+            spawn(P, b + L, e, dstB, true, piv_ord, sg.pivot_v, nb, sg.depth + 1, perturb,
                   used ? -1 : (int)sid);
         } else {
             if (tid == 0) sh.s_part_left++;
@@ -323,27 +672,22 @@ struct Sorter {
             if (srcB) {
                 // lefts were written straight into A during the pass
                 if (tid == 0 && L) finish_keys(P, (unsigned long long)L);
-                __syncthreads();
+                csync();
             } else {
-                used = fill_final(P, sh, b, b + L, sg.pivot, sg.pivot_v, (int)sid);
+                used = fill_final(P, b, b + L, piv_ord, sg.pivot_v, (int)sid);
             }
-            spawn(P, sh, sk, sv, b + L, e, dstB, true, sg.pivot, sg.pivot_v, sg.budget, sg.depth + 1, false,
+            spawn(P, b + L, e, dstB, true, piv_ord, sg.pivot_v, sg.budget, sg.depth + 1, false,
                   used ? -1 : (int)sid);
         }
     }
 
-    // ---- K2/K3: one partition tile ------------------------------------------------------------
-    __device__ static void part_tile(const Params &P, Shared &sh, U *sk, uint32_t *sv, U *ck, uint32_t *cv,
-                                     uint32_t sid, uint32_t tile, unsigned &phase) {
-        const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-        const Seg &sg = sh.seg;
+    // ---- thread 0: issue the TMA bulk load of tile `tile` of segment `sg` into the stage ---------------
+    __device__ static void issue_load(const Params &P, const Seg &sg, uint32_t tile) {
+        Shared &sh = g_sh;
         const int64_t b = sg.begin, e = sg.end;
         const bool srcB = sg.info & I_SRC_B;
-        const bool left_mode = sg.info & I_LEFT;
         const U *src = (const U *)(srcB ? P.b_keys : P.a_keys);
-        U *dst = (U *)(srcB ? P.a_keys : P.b_keys);
         const uint32_t *srcv = srcB ? P.b_vals : P.a_vals;
-        uint32_t *dstv = srcB ? P.a_vals : P.b_vals;
         const int64_t tbase = (b / TILE + tile) * (int64_t)TILE;
         const int64_t lo = b > tbase ? b : tbase;
         const int64_t hi = e < tbase + TILE ? e : tbase + TILE;
@@ -351,145 +695,298 @@ struct Sorter {
         const int64_t lo_al = lo & ~(int64_t)(AL - 1);
         int64_t hi_al = (hi + AL - 1) & ~(int64_t)(AL - 1);
         if (hi_al > nfl) hi_al = nfl;
-        const bool bulk = hi_al > lo_al;
-        if (tid == 0 && bulk) {
-            const unsigned kb = (unsigned)((hi_al - lo_al) * sizeof(U));
-            const unsigned vb = KV ? (unsigned)((hi_al - lo_al) * 4) : 0u;
-            fence_proxy_async();
-            mbar_expect_tx(&sh.bar, kb + vb);
-            bulk_g2s(sk + (lo_al - tbase), src + lo_al, kb, &sh.bar);
-            if (KV) bulk_g2s(sv + (lo_al - tbase), srcv + lo_al, vb, &sh.bar);
-        }
+        U *sk = B::stage();
+        uint32_t *sv = KV ? B::vstage() : nullptr;
         // the array's last < 16 bytes cannot be bulk-copied: scalar loads
-        for (int64_t g = (hi_al > lo ? hi_al : lo) + tid; g < hi; g += THREADS) {
+        for (int64_t g = (hi_al > lo ? hi_al : lo); g < hi; ++g) {
             sk[g - tbase] = ldcg(src + g);
             if (KV) sv[g - tbase] = ldcg(srcv + g);
         }
-        if (bulk) {
-            mbar_wait(&sh.bar, phase);
-            phase ^= 1;
-        }
-        __syncthreads();
-
-        // classify: left = key < pivot (partition_right, equals go right, partition.py:76-77)
-        //           left = key <= pivot (partition_left, equals go left, partition.py:134-135)
-        // Pass 1 counts per warp with ballot/popc; pass 2 recomputes the same ballots and
-        // scatters into the compaction buffer, so no per-key state lives in registers.
-        const uint64_t piv = sg.pivot;
-        const uint32_t pv = sg.pivot_v;
-        const unsigned ltm = lanemask_lt();
-        const int lo_i = (int)(lo - tbase), hi_i = (int)(hi - tbase);
-        int wl = 0, wv = 0, eqc = 0;
-#pragma unroll 4
-        for (int j = 0; j < ITEMS; ++j) {
-            const int idx = j * THREADS + tid;
-            const bool valid = idx >= lo_i && idx < hi_i;
-            const uint64_t ok = (uint64_t)O::to(sk[idx]);
-            const uint32_t v = KV ? sv[idx] : 0u;
-            const bool isl = valid && (left_mode ? !pless<KV>(piv, pv, ok, v) : pless<KV>(ok, v, piv, pv));
-            eqc += (valid && ok == piv && (!KV || v == pv)) ? 1 : 0;
-            wl += __popc(__ballot_sync(0xffffffffu, isl));
-            wv += __popc(__ballot_sync(0xffffffffu, valid));
-        }
-        eqc = __reduce_add_sync(0xffffffffu, eqc);
-        if (lane == 0) {
-            sh.wl[warp] = wl;
-            sh.wv[warp] = wv;
-            sh.weq[warp] = eqc;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            int offL = 0, offR = 0, E = 0;
-#pragma unroll
-            for (int w = 0; w < WARPS; ++w) {
-                sh.wloff[w] = offL;
-                sh.wroff[w] = offR;
-                offL += sh.wl[w];
-                offR += sh.wv[w] - sh.wl[w];
-                E += sh.weq[w];
-            }
-            Seg *gs = &P.segs[sid];
-            sh.L = offL;
-            sh.R = offR;
-            // one atomic per side per CTA: the left run grows up from `begin`, the right
-            // run grows down from `end`
-            sh.lOff = offL ? (long long)atomicAdd(&gs->cnt_left, (unsigned long long)offL) : 0;
-            sh.rOff = offR ? (long long)atomicAdd(&gs->cnt_right, (unsigned long long)offR) : 0;
-            if (!left_mode && E) atomicAdd(&gs->cnt_eq, (unsigned long long)E);
-            sh.s_tiles++;
-            const bool write_left = !left_mode || srcB;
-            sh.s_bytes += (unsigned long long)ELEM_BYTES * (offL + offR) +
-                          (unsigned long long)ELEM_BYTES * (offR + (write_left ? offL : 0));
-        }
-        __syncthreads();
-        const int L = (int)sh.L;
-        {
-            int lrun = sh.wloff[warp], rrun = L + sh.wroff[warp];
-#pragma unroll 4
-            for (int j = 0; j < ITEMS; ++j) {
-                const int idx = j * THREADS + tid;
-                const bool valid = idx >= lo_i && idx < hi_i;
-                const U k = sk[idx];
-                const uint64_t ok = (uint64_t)O::to(k);
-                const uint32_t v = KV ? sv[idx] : 0u;
-                const bool isl = valid && (left_mode ? !pless<KV>(piv, pv, ok, v) : pless<KV>(ok, v, piv, pv));
-                const unsigned bl = __ballot_sync(0xffffffffu, isl);
-                const unsigned br = __ballot_sync(0xffffffffu, valid && !isl);
-                if (valid) {
-                    const int pos = isl ? lrun + __popc(bl & ltm) : rrun + __popc(br & ltm);
-                    ck[pos] = k;
-                    if (KV) cv[pos] = v;
-                }
-                lrun += __popc(bl);
-                rrun += __popc(br);
-            }
-        }
-        __syncthreads();
-        const int R = (int)sh.R;
-        const long long lOff = sh.lOff, rOff = sh.rOff;
-        if (L && (!left_mode || srcB)) {
-            store_run<U>(dst + b + lOff, L, [&](int64_t i) { return ck[i]; });
-            if (KV) store_run<uint32_t>(dstv + b + lOff, L, [&](int64_t i) { return cv[i]; });
-        }
-        if (R) {
-            store_run<U>(dst + e - rOff - R, R, [&](int64_t i) { return ck[L + i]; });
-            if (KV) store_run<uint32_t>(dstv + e - rOff - R, R, [&](int64_t i) { return cv[L + i]; });
-        }
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) {
-            unsigned old = atomicAdd(&P.segs[sid].tiles_done, 1u);
-            sh.last = (old == sg.ntiles - 1);
-        }
-        __syncthreads();
-        if (sh.last) {
-            __threadfence();
-            finalize_part(P, sh, sk, sv, sid);
+        const unsigned kb = hi_al > lo_al ? (unsigned)((hi_al - lo_al) * sizeof(U)) : 0u;
+        const unsigned vb = (KV && hi_al > lo_al) ? (unsigned)((hi_al - lo_al) * 4) : 0u;
+        fence_proxy_async();
+        mbar_expect_tx(&sh.bar, kb + vb);  // the stage barrier's single arrival (+ bytes, maybe 0)
+        if (kb) {
+            bulk_g2s(sk + (lo_al - tbase), src + lo_al, kb, &sh.bar);
+            if (KV) bulk_g2s(sv + (lo_al - tbase), srcv + lo_al, vb, &sh.bar);
         }
     }
 
-    __device__ static void fill_tile(const Params &P, Shared &sh, uint32_t tile) {
+    // ---- K2/K3: one partition tile (compute warps) ------------------------------------------------
+    __device__ __forceinline__ static void ldvec(const U *s, int q, U (&x)[VEC]) {
+        if constexpr (sizeof(U) == 4) {
+            const uint4 y = reinterpret_cast<const uint4 *>(s)[q];
+            x[0] = y.x;
+            x[1] = y.y;
+            x[2] = y.z;
+            x[3] = y.w;
+        } else {
+            const ulonglong2 y = reinterpret_cast<const ulonglong2 *>(s)[q];
+            x[0] = y.x;
+            x[1] = y.y;
+        }
+    }
+
+    // Per-thread classification of ITEMS keys held in registers.  Thread t owns the VEC-key
+    // vectors q = jj*THREADS + t; lmask/vmask record left/valid per item.
+    // Per-thread classification of the ITEMS keys of thread t (the VEC-key vectors
+    // q = jj*THREADS + t); lmask/vmask record left/valid per item.
+    template <bool FULL>
+    __device__ __forceinline__ static void classify(const U *sk, const uint32_t *sv, int lo_i, int hi_i, U piv,
+                                                    uint32_t pv, bool left_mode, bool count_eq, unsigned &lmask,
+                                                    unsigned &vmask, int &eqc) {
+        const int tid = threadIdx.x;
+#pragma unroll
+        for (int jj = 0; jj < ITEMS / VEC; ++jj) {
+            const int q = jj * THREADS + tid;
+            U kk[VEC];
+            ldvec(sk, q, kk);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                const int r = jj * VEC + e;
+                const int idx = q * VEC + e;
+                const uint32_t v = KV ? sv[idx] : 0u;
+                const bool valid = FULL || (idx >= lo_i && idx < hi_i);
+                const bool isl = valid && (left_mode ? !lt_raw(piv, pv, kk[e], v) : lt_raw(kk[e], v, piv, pv));
+                lmask |= (unsigned)isl << r;
+                if (!FULL) vmask |= (unsigned)valid << r;
+                if (count_eq) eqc += (valid && kk[e] == piv && (!KV || v == pv)) ? 1 : 0;
+            }
+        }
+        if (FULL) vmask = (1u << ITEMS) - 1;
+    }
+
+    // Branch-free compaction of this thread's keys into kc: lefts from li, rights from ri.
+    template <bool FULL>
+    __device__ __forceinline__ static void scatter(const U *sk, const uint32_t *sv, U *kc, uint32_t *vc,
+                                                   unsigned lmask, unsigned vmask, int li, int ri) {
+        const int tid = threadIdx.x;
+#pragma unroll
+        for (int jj = 0; jj < ITEMS / VEC; ++jj) {
+            const int q = jj * THREADS + tid;
+            U kk[VEC];
+            ldvec(sk, q, kk);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                const int r = jj * VEC + e;
+                const bool isl = (lmask >> r) & 1u;
+                const bool valid = FULL || ((vmask >> r) & 1u);
+                const int pos = isl ? li : ri;
+                if (valid) {
+                    kc[pos] = kk[e];
+                    if (KV) vc[pos] = sv[q * VEC + e];
+                }
+                li += isl;
+                ri += valid && !isl;
+            }
+        }
+    }
+
+    // Partition the tile in stage `s`; returns after the stores are issued.  Releases the stage
+    // (empty barrier) as soon as its buffer has been consumed.
+    //   left = key <  pivot  (partition_right: equals go right, partition.py:76-77)
+    //   left = key <= pivot  (partition_left: equals go left, partition.py:134-135)
+    // Each thread counts its own keys; one block-wide exclusive scan (packed left|right<<16)
+    // gives every thread its slots in the compaction buffer: lefts fill kc from the front,
+    // rights follow them.  One 64-bit atomic per CTA reserves both output runs.
+    // One partition tile of the current task (sh.seg), whose TMA load is in flight in the stage.
+    // After the stage is consumed thread 0 starts the next load (next tile of this chunk, or the
+    // first tile of the already-claimed next task), so the load overlaps this tile's reservation
+    // atomic and stores.
+    __device__ static void part_tile(const Params &P, uint32_t sid, uint32_t tile, unsigned &phase) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
         const Seg &sg = sh.seg;
+        const int64_t b = sg.begin, e = sg.end;
+        const bool srcB = sg.info & I_SRC_B;
+        const bool left_mode = sg.info & I_LEFT;
+        const bool count_eq = (sg.info & I_COUNT_EQ) && !left_mode;
+        const bool packed = (e - b) < (1ll << 32);
+        const int64_t tbase = (b / TILE + tile) * (int64_t)TILE;
+        const int64_t lo = b > tbase ? b : tbase;
+        const int64_t hi = e < tbase + TILE ? e : tbase + TILE;
+        const U *sk = B::stage();
+        const uint32_t *sv = KV ? B::vstage() : nullptr;
+        const U piv = (U)sg.pivot;
+        const uint32_t pv = sg.pivot_v;
+        const int lo_i = (int)(lo - tbase), hi_i = (int)(hi - tbase);
+        mbar_wait(&sh.bar, phase);
+        phase ^= 1;
+        unsigned lmask = 0, vmask = 0;
+        int eqc = 0;
+        if (lo_i == 0 && hi_i == TILE)
+            classify<true>(sk, sv, lo_i, hi_i, piv, pv, left_mode, count_eq, lmask, vmask, eqc);
+        else
+            classify<false>(sk, sv, lo_i, hi_i, piv, pv, left_mode, count_eq, lmask, vmask, eqc);
+        const int nl = __popc(lmask), nv = __popc(vmask);
+        const uint32_t mine = (uint32_t)nl | ((uint32_t)(nv - nl) << 16);
+        uint32_t inc = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (count_eq) eqc = __reduce_add_sync(0xffffffffu, eqc);
+        if (lane == 31) {
+            sh.scan[warp] = inc;
+            sh.weq[warp] = eqc;
+        }
+        csync();
+        uint32_t wpre = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) {
+            const uint32_t x = sh.scan[w];
+            wpre += (w < warp) ? x : 0u;
+            tot += x;
+        }
+        const int L = (int)(tot & 0xFFFF), R = (int)(tot >> 16);
+        unsigned long long res_lr = 0, res_r = 0;
+        if (tid == 0) {
+            // one atomic per CTA reserves both runs (left grows up from `begin`, right grows down
+            // from `end`); its result is consumed only after the scatter below
+            Seg *gs = &P.segs[sid];
+            if (packed) {
+                res_lr = atomicAdd(&gs->cnt_left, (unsigned long long)L | ((unsigned long long)R << 32));
+            } else {
+                res_lr = atomicAdd(&gs->cnt_left, (unsigned long long)L);
+                res_r = atomicAdd(&gs->cnt_right, (unsigned long long)R);
+            }
+            if (count_eq) {
+                int E = 0;
+#pragma unroll
+                for (int w = 0; w < WARPS; ++w) E += sh.weq[w];
+                if (E) atomicAdd(&gs->cnt_eq, (unsigned long long)E);
+            }
+        }
+        const uint32_t pre = wpre + inc - mine;
+        const int li0 = (int)(pre & 0xFFFF), ri0 = L + (int)(pre >> 16);
+        U *kc = B::kc();
+        uint32_t *vc = KV ? B::vc() : nullptr;
+        if (vmask == (1u << ITEMS) - 1)
+            scatter<true>(sk, sv, kc, vc, lmask, vmask, li0, ri0);
+        else
+            scatter<false>(sk, sv, kc, vc, lmask, vmask, li0, ri0);
+        csync();  // stage consumed
+        if (tid == 0) {
+            prefetch_next(P, tile);
+            if (packed) {
+                sh.lOff = (long long)(res_lr & 0xFFFFFFFFull);
+                sh.rOff = (long long)(res_lr >> 32);
+            } else {
+                sh.lOff = (long long)res_lr;
+                sh.rOff = (long long)res_r;
+            }
+            sh.s_tiles++;
+            const bool write_left = !left_mode || srcB;
+            sh.s_bytes += (unsigned long long)ELEM_BYTES * (L + R) +
+                          (unsigned long long)ELEM_BYTES * (R + (write_left ? L : 0));
+        }
+        csync();
+        const long long lOff = sh.lOff, rOff = sh.rOff;
+        U *dst = (U *)(srcB ? P.a_keys : P.b_keys);
+        uint32_t *dstv = srcB ? P.a_vals : P.b_vals;
+        if (L && (!left_mode || srcB)) {
+            store_run<U>(dst + b + lOff, L, [&](int i) { return kc[i]; });
+            if (KV) store_run<uint32_t>(dstv + b + lOff, L, [&](int i) { return vc[i]; });
+        }
+        if (R) {
+            store_run<U>(dst + e - rOff - R, R, [&](int i) { return kc[L + i]; });
+            if (KV) store_run<uint32_t>(dstv + e - rOff - R, R, [&](int i) { return vc[L + i]; });
+        }
+    }
+
+    // thread 0, after tile `tile` of the current task consumed the stage: start the next load
+    __device__ static void prefetch_next(const Params &P, uint32_t tile) {
+        Shared &sh = g_sh;
+        const uint32_t chunk_end = min(((uint32_t)(sh.task & 0x7FFFFF) + 1) * CHUNK, sh.seg.ntiles);
+        if (tile + 1 < chunk_end) {
+            issue_load(P, sh.seg, tile + 1);
+            return;
+        }
+        if (sh.nstate == 1) poll_next(P);
+        if (sh.nstate == 2 && ((uint32_t)(sh.ntask >> 45) & 7u) == T_PART)
+            issue_load(P, sh.nseg, ((uint32_t)sh.ntask & 0x7FFFFF) * CHUNK);
+    }
+
+    // thread 0: non-blocking poll of the claimed next ring position
+    __device__ static void poll_next(const Params &P) {
+        Shared &sh = g_sh;
+        const uint64_t mask = (1ull << P.log_q) - 1;
+        const unsigned long long pos = sh.npos;
+        const uint64_t w = ld_acquire_u64(P.ring + (pos & mask));
+        if ((w >> 48) == ((pos >> P.log_q) & 0xFFFFull)) {
+            const uint32_t sid = (uint32_t)(w >> 23) & 0x3FFFFF;
+            const ulonglong2 *gsrc = reinterpret_cast<const ulonglong2 *>(&P.segs[sid]);
+            ulonglong2 *sdst = reinterpret_cast<ulonglong2 *>(&sh.nseg);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sdst[q] = __ldcg(gsrc + q);
+            sh.ntask = w;
+            sh.nstate = 2;
+        }
+    }
+
+    // thread 0: make the claimed next task current (blocking until it is published or the sort is
+    // done), start its first load if it was not prefetched, and claim the position after it.
+    __device__ static void advance(const Params &P) {
+        Shared &sh = g_sh;
+        if (sh.nstate == 1) {
+            const uint64_t t0 = globaltimer_ns();
+            unsigned ns = 32;
+            for (;;) {
+                poll_next(P);
+                if (sh.nstate == 2) break;
+                if (ld_volatile_u32(&P.st->done)) {
+                    sh.nstate = 3;
+                    break;
+                }
+                if (globaltimer_ns() - t0 > WATCHDOG_NS) {  // no task for 10 s: report, never hang
+                    fail(P, -8);
+                    sh.nstate = 3;
+                    break;
+                }
+                __nanosleep(ns);
+                if (ns < 1024) ns <<= 1;
+            }
+            if (sh.nstate == 2 && ((uint32_t)(sh.ntask >> 45) & 7u) == T_PART)
+                issue_load(P, sh.nseg, ((uint32_t)sh.ntask & 0x7FFFFF) * CHUNK);
+        }
+        if (sh.nstate == 3) {
+            sh.task = 0;
+            return;
+        }
+        sh.task = sh.ntask;
+        sh.seg = sh.nseg;
+        // claim the following position now: its atomic overlaps the whole current task
+        sh.npos = atomicAdd(&P.st->q_head, 1ull);
+        sh.nstate = 1;
+    }
+
+    __device__ static void fill_tile(const Params &P, const Seg &sg, uint32_t tile) {
+        Shared &sh = g_sh;
         const int64_t tbase = (sg.begin / TILE + tile) * (int64_t)TILE;
         const int64_t lo = sg.begin > tbase ? sg.begin : tbase;
         const int64_t hi = sg.end < tbase + TILE ? sg.end : tbase + TILE;
         const U raw = O::from((U)sg.pivot);
         const uint32_t pv = sg.pivot_v;
-        store_run<U>((U *)P.a_keys + lo, hi - lo, [&](int64_t) { return raw; });
-        if (KV) store_run<uint32_t>(P.a_vals + lo, hi - lo, [&](int64_t) { return pv; });
+        store_run<U>((U *)P.a_keys + lo, (int)(hi - lo), [&](int) { return raw; });
+        if (KV) store_run<uint32_t>(P.a_vals + lo, (int)(hi - lo), [&](int) { return pv; });
         __threadfence();
-        __syncthreads();
+        csync();
         if (threadIdx.x == 0) {
             sh.s_bytes += (unsigned long long)ELEM_BYTES * (hi - lo);
             finish_keys(P, (unsigned long long)(hi - lo));
         }
     }
 
-    __device__ static void zero_counters(Shared &sh) {
+    __device__ static void zero_counters() {
+        Shared &sh = g_sh;
         sh.s_part_right = sh.s_part_left = sh.s_bad = sh.s_fallback = sh.s_base = sh.s_tiles = sh.s_bytes = 0;
         sh.s_max_depth = 0;
+        sh.s_cyc_wait = sh.s_cyc_work = sh.s_cyc_base = sh.s_cyc_spawn = 0;
+        sh.s_sch_retire = sh.s_sch_claim = sh.s_sch_fetch = sh.s_sch_idle = 0;
     }
-    __device__ static void flush_counters(const Params &P, Shared &sh) {
+    __device__ static void flush_counters(const Params &P) {
+        Shared &sh = g_sh;
         State *st = P.st;
         if (sh.s_part_right) atomicAdd(&st->c_part_right, sh.s_part_right);
         if (sh.s_part_left) atomicAdd(&st->c_part_left, sh.s_part_left);
@@ -499,12 +996,20 @@ struct Sorter {
         if (sh.s_tiles) atomicAdd(&st->c_tiles, sh.s_tiles);
         if (sh.s_bytes) atomicAdd(&st->c_bytes, sh.s_bytes);
         if (sh.s_max_depth) atomicMax(&st->c_max_depth, (unsigned long long)sh.s_max_depth);
+        atomicAdd(&st->c_cyc_wait, sh.s_cyc_wait);
+        atomicAdd(&st->c_cyc_work, sh.s_cyc_work);
+        atomicAdd(&st->c_cyc_base, sh.s_cyc_base);
+        atomicAdd(&st->c_cyc_spawn, sh.s_cyc_spawn);
+        atomicAdd(&st->c_sch_retire, sh.s_sch_retire);
+        atomicAdd(&st->c_sch_claim, sh.s_sch_claim);
+        atomicAdd(&st->c_sch_fetch, sh.s_sch_fetch);
+        atomicAdd(&st->c_sch_idle, sh.s_sch_idle);
     }
 };
 
 // ---- K4: adjacent-compare reduction with early exit ---------------------------------------------
 template <class U, bool FLOAT, bool KV>
-__global__ void __launch_bounds__(THREADS) k_check(Params P) {
+__global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Params P) {
     using O = Ord<U, FLOAT>;
     __shared__ unsigned s_stop;
     const int tid = threadIdx.x;
@@ -517,18 +1022,15 @@ __global__ void __launch_bounds__(THREADS) k_check(Params P) {
         __syncthreads();
         if (s_stop) break;
         unsigned bits = 0;
-        const int64_t i0 = c0 + (int64_t)tid * ITEMS;
-        if (i0 < n - 1) {
-            uint64_t prev = (uint64_t)O::to(a[i0]);
-            uint32_t pvv = KV ? P.a_vals[i0] : 0u;
-            const int64_t lim = (i0 + ITEMS < n - 1) ? i0 + ITEMS : n - 1;
-            for (int64_t i = i0 + 1; i <= lim; ++i) {
-                const uint64_t cur = (uint64_t)O::to(a[i]);
-                const uint32_t cv = KV ? P.a_vals[i] : 0u;
-                bits |= pless<KV>(cur, cv, prev, pvv) ? 1u : 0u;
-                bits |= pless<KV>(prev, pvv, cur, cv) ? 2u : 0u;
-                prev = cur;
-                pvv = cv;
+        // each thread compares ITEMS pairs; lanes read adjacent elements (coalesced per slot)
+#pragma unroll 4
+        for (int j = 0; j < ITEMS; ++j) {
+            const int64_t i = c0 + (int64_t)j * THREADS + tid;
+            if (i < n - 1) {
+                const uint64_t x = (uint64_t)O::to(a[i]), y = (uint64_t)O::to(a[i + 1]);
+                const uint32_t xv = KV ? P.a_vals[i] : 0u, yv = KV ? P.a_vals[i + 1] : 0u;
+                bits |= pless<KV>(y, yv, x, xv) ? 1u : 0u;
+                bits |= pless<KV>(x, xv, y, yv) ? 2u : 0u;
             }
         }
         bits = __reduce_or_sync(0xffffffffu, bits);
@@ -542,16 +1044,13 @@ __global__ void __launch_bounds__(THREADS) k_check(Params P) {
 
 // ---- init: decide from K4, reverse flag, root segment --------------------------------------------
 template <class U, bool FLOAT, bool KV>
-__global__ void __launch_bounds__(THREADS) k_init(Params P) {
+__global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params P) {
     using S = Sorter<U, FLOAT, KV>;
-    extern __shared__ __align__(128) unsigned char dsm[];
-    __shared__ Shared sh;
+    Shared &sh = g_sh;
     __shared__ int s_action;
-    U *sk = reinterpret_cast<U *>(dsm);
-    uint32_t *sv = reinterpret_cast<uint32_t *>(dsm + 2 * sizeof(U) * TILE);
     const int tid = threadIdx.x;
     if (tid == 0) {
-        S::zero_counters(sh);
+        S::zero_counters();
         const unsigned bits = P.st->check_bits;
         int action = 0;  // 0 = sort, 1 = done (sorted), 2 = reverse
         if (P.n <= 1) action = 1;
@@ -571,25 +1070,23 @@ __global__ void __launch_bounds__(THREADS) k_init(Params P) {
     __syncthreads();
     if (s_action == 0) {
         int budget = P.budget0;
-        if (budget < 0) {  // driver.py:263: n.bit_length() - 1
-            budget = 63 - __clzll((long long)P.n);
-        }
-        S::spawn(P, sh, sk, sv, 0, P.n, false, false, 0, 0, budget, 0, false, -1);
+        if (budget < 0) budget = 63 - __clzll((long long)P.n);  // driver.py:263: n.bit_length() - 1
+        S::spawn(P, 0, P.n, false, false, 0, 0, budget, 0, false, -1);
     }
     __syncthreads();
-    if (tid == 0) S::flush_counters(P, sh);
+    if (tid == 0) S::flush_counters(P);
 }
 
-// ---- K6: the persistent segment-queue sorter -----------------------------------------------------
+// ---- K6: the persistent segment-queue sorter --------------------------------------------------------
+template <class U, bool KV>
+constexpr int sort_min_blocks() {
+    return Bufs<U, KV>::bytes() <= 56 * 1024 ? 4 : (Bufs<U, KV>::bytes() <= 108 * 1024 ? 2 : 1);
+}
+
 template <class U, bool FLOAT, bool KV>
-__global__ void __launch_bounds__(THREADS) k_sort(Params P) {
+__global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(const __grid_constant__ Params P) {
     using S = Sorter<U, FLOAT, KV>;
-    extern __shared__ __align__(128) unsigned char dsm[];
-    __shared__ Shared sh;
-    U *sk = reinterpret_cast<U *>(dsm);
-    U *ck = sk + TILE;
-    uint32_t *sv = reinterpret_cast<uint32_t *>(dsm + 2 * sizeof(U) * TILE);
-    uint32_t *cv = sv + TILE;
+    Shared &sh = g_sh;
     const int tid = threadIdx.x;
 
     // K4 reverse: a non-increasing input is reversed in place (one read + one write pass)
@@ -610,58 +1107,54 @@ __global__ void __launch_bounds__(THREADS) k_sort(Params P) {
         return;
     }
     if (tid == 0) {
-        S::zero_counters(sh);
+        S::zero_counters();
         mbar_init(&sh.bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        sh.npos = atomicAdd(&P.st->q_head, 1ull);
+        sh.nstate = 1;
+        S::advance(P);
     }
     __syncthreads();
     unsigned phase = 0;
-    const uint64_t mask = (1ull << P.log_q) - 1;
+    long long c_prev = clock64();
     for (;;) {
-        if (tid == 0) {
-            const unsigned long long pos = atomicAdd(&P.st->q_head, 1ull);
-            const uint64_t want = (pos >> P.log_q) & 0xFFFFull;
-            const uint64_t *slot = P.ring + (pos & mask);
-            uint64_t w;
-            unsigned ns = 32;
-            const uint64_t t0 = globaltimer_ns();
-            for (;;) {
-                w = ld_acquire_u64(slot);
-                if ((w >> 48) == want) break;
-                if (ld_volatile_u32(&P.st->done)) {
-                    w = 0;
-                    break;
-                }
-                __nanosleep(ns);
-                if (ns < 1024) ns <<= 1;
-                if (globaltimer_ns() - t0 > WATCHDOG_NS) {  // no task for 10 s: report, never hang
-                    S::fail(P, -8);
-                    w = 0;
-                    break;
-                }
-            }
-            sh.task = w;
-            if (w) {
-                const uint32_t sid = (uint32_t)(w >> 23) & 0x3FFFFF;
-                const ulonglong2 *gsrc = reinterpret_cast<const ulonglong2 *>(&P.segs[sid]);
-                ulonglong2 *sdst = reinterpret_cast<ulonglong2 *>(&sh.seg);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) sdst[q] = __ldcg(gsrc + q);
-            }
-        }
-        __syncthreads();
         const uint64_t w = sh.task;
         if (!w) break;
         const uint32_t type = (uint32_t)(w >> 45) & 7u;
         const uint32_t sid = (uint32_t)(w >> 23) & 0x3FFFFF;
-        const uint32_t tile = (uint32_t)w & 0x7FFFFF;
-        if (type == T_PART)
-            S::part_tile(P, sh, sk, sv, ck, cv, sid, tile, phase);
-        else
-            S::fill_tile(P, sh, tile);
-        __syncthreads();
+        if (type == T_PART) {
+            const uint32_t t0 = ((uint32_t)w & 0x7FFFFF) * CHUNK;
+            const uint32_t t1 = min(t0 + CHUNK, sh.seg.ntiles);
+            for (uint32_t t = t0; t < t1; ++t) S::part_tile(P, sid, t, phase);
+            // retire the chunk: one gpu-scope fence per thread, one counter update per CTA
+            __threadfence();
+            csync();
+            if (tid == 0) {
+                const long long c = clock64();
+                const unsigned old = atomicAdd(&P.segs[sid].tiles_done, t1 - t0);
+                sh.last = (old + (t1 - t0) == sh.seg.ntiles);
+                sh.s_sch_retire += clock64() - c;
+            }
+            csync();
+            if (sh.last) {
+                __threadfence();
+                S::finalize_part(P, sh.seg, sid);
+            }
+        } else {  // T_FILL
+            S::fill_tile(P, sh.seg, (uint32_t)w & 0x7FFFFF);
+        }
+        csync();
+        if (tid == 0) {
+            const long long c = clock64();
+            sh.s_cyc_work += c - c_prev;
+            S::advance(P);
+            const long long c2 = clock64();
+            sh.s_cyc_wait += c2 - c;
+            c_prev = c2;
+        }
+        csync();
     }
-    if (tid == 0) S::flush_counters(P, sh);
+    if (tid == 0) S::flush_counters(P);
 }
 
 }  // namespace pdq
