@@ -313,8 +313,10 @@ def run_ours(args, rank, world, local_rank):
                 "bytes_per_key": bytes_launch / n,
                 "kernel_ms": ks_ms,
                 "kernel_share_of_step": ks_ms / (total_ms / K),
+                "whole_sort_alg_GBps": (bytes_launch + stats["bytes_base"] + stats["bytes_check"]) / (total_ms / K / 1e3) / 1e9,
+                "whole_sort_frac": (bytes_launch + stats["bytes_base"] + stats["bytes_check"]) / (total_ms / K / 1e3) / 1e9 / peak,
             },
-            "gpu_launches": 3 * K,
+            "gpu_launches": 4 * K,
             "device_counters": stats,
             "clocks": clocks.summary(),
             "wall_s_timed_region": t_wall,

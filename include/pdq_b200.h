@@ -91,6 +91,7 @@ typedef struct pdq_stats {
     int64_t sched_claim;            /*   ... claiming ring positions */
     int64_t sched_fetch;            /*   ... polling the ring, copying descriptors, issuing loads */
     int64_t sched_idle;             /*   ... sleeping with nothing to do */
+    int64_t bytes_base;             /* algorithmic bytes of the K7 base-case kernel (not in bytes_algorithmic) */
 } pdq_stats;
 
 /* Fill `cfg` with the reference defaults (driver.py:55-63) and GPU defaults. */
@@ -111,8 +112,8 @@ int pdq_sort(void *keys, int dtype, uint32_t *payload, int64_t n, const pdq_conf
              void *workspace, size_t workspace_bytes, void *stream);
 
 /* pdq_sort() that also records two caller-owned CUDA events (cudaEvent_t, may be NULL) on
- * `stream` immediately before and after the persistent sorter kernel, so a profiler-free
- * caller can time the dominant kernel alone (bench.py's roofline figure). */
+ * `stream` immediately before and after the persistent partition kernel (K6/K1-K5), so a
+ * profiler-free caller can time the dominant kernel alone (bench.py's roofline figure). */
 int pdq_sort_ex(void *keys, int dtype, uint32_t *payload, int64_t n, const pdq_config *cfg,
                 void *workspace, size_t workspace_bytes, void *stream, void *event_sort_begin,
                 void *event_sort_end);

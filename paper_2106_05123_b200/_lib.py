@@ -12,7 +12,7 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libpdq_b200.so")
+LIB_PATH = os.environ.get("PDQ_LIB") or os.path.join(HERE, "libpdq_b200.so")
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 
@@ -82,6 +82,7 @@ STAT_FIELDS = (
     "sched_claim",
     "sched_fetch",
     "sched_idle",
+    "bytes_base",
 )
 
 

@@ -59,7 +59,8 @@ namespace {
 constexpr int MIN_BASE = 1024;
 
 struct Layout {
-    size_t b_keys, b_vals, state, segs, ring, total;
+    size_t b_keys, b_vals, state, segs, ring, leaves, total;
+    uint64_t leaf_cap;
     uint32_t seg_cap;
     int log_q;
 };
@@ -99,6 +100,10 @@ Layout layout(int dtype, int has_payload, int64_t n) {
     L.log_q = lq;
     L.ring = off;
     off += a256((size_t)(1ull << lq) * 8);
+    // leaves are disjoint segments of more than 64 keys (smaller ones are sorted in place)
+    L.leaf_cap = (uint64_t)n / 64 + 16;
+    L.leaves = off;
+    off += a256((size_t)L.leaf_cap * 8);
     L.total = off;
     return L;
 }
@@ -106,6 +111,7 @@ Layout layout(int dtype, int has_payload, int64_t n) {
 struct LaunchInfo {
     int sms = 0;
     int occ = 0;
+    int occ_base = 0;
 };
 
 template <class U, bool FLOAT, bool KV>
@@ -130,6 +136,14 @@ cudaError_t prepare(LaunchInfo &li) {
         if ((e = cudaFuncSetAttribute(k_init<U, FLOAT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) !=
             cudaSuccess)
             return e;
+        const int smb = BaseBufs<U, KV>::bytes();
+        if ((e = cudaFuncSetAttribute(k_base<U, FLOAT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb)) !=
+            cudaSuccess)
+            return e;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached.occ_base, k_base<U, FLOAT, KV>, THREADS, smb)) !=
+            cudaSuccess)
+            return e;
+        if (cached.occ_base < 1) cached.occ_base = 1;
         if ((e = cudaDeviceGetAttribute(&cached.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached.occ, k_sort<U, FLOAT, KV>, THREADS, sm)) !=
             cudaSuccess)
@@ -158,6 +172,7 @@ int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEven
     if (ev0) cudaEventRecord(ev0, s);
     k_sort<U, FLOAT, KV><<<(unsigned)(li.sms * li.occ), THREADS, sm, s>>>(P);
     if (ev1) cudaEventRecord(ev1, s);
+    k_base<U, FLOAT, KV><<<(unsigned)(li.sms * li.occ_base), THREADS, BaseBufs<U, KV>::bytes(), s>>>(P);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "launch: %s", cudaGetErrorString(e));
     return PDQ_OK;
@@ -223,6 +238,8 @@ extern "C" int pdq_sort_ex(void *keys, int dtype, uint32_t *payload, int64_t n, 
     P.base_size = cfg.base_case_size;
     P.budget0 = cfg.bad_budget;
     P.debug_depth = cfg.reserved[0];
+    P.leaves = (uint64_t *)(ws + L.leaves);
+    P.leaf_cap = L.leaf_cap;
 
     const bool kv = payload != nullptr;
     switch (dtype) {
@@ -255,6 +272,7 @@ extern "C" int pdq_sort_finish(void *workspace, pdq_stats *out, void *stream) {
         out->segments = (int64_t)st.seg_alloc;
         out->status = (int64_t)st.status;
         out->bytes_check = (int64_t)st.c_bytes_check;
+        out->bytes_base = (int64_t)st.c_bytes_base;
         out->cycles_wait = (int64_t)st.c_cyc_wait;
         out->cycles_work = (int64_t)st.c_cyc_work;
         out->cycles_base = (int64_t)st.c_cyc_base;

@@ -78,8 +78,10 @@ struct __align__(128) State {
     unsigned int pad_c;
     unsigned long long pad_d[12];
     // counters (pdq_stats order)
+    unsigned long long leaf_count;  // queued base-case segments (K7 kernel input)
+    unsigned long long leaf_next;   // K7 kernel claim counter
     unsigned long long c_part_right, c_part_left, c_bad, c_fallback, c_base, c_max_depth, c_tiles,
-        c_bytes, c_bytes_check;
+        c_bytes, c_bytes_check, c_bytes_base;
     unsigned long long c_cyc_wait, c_cyc_work, c_cyc_base, c_cyc_spawn;  // SM cycles by phase (thread 0)
     unsigned long long c_sch_retire, c_sch_claim, c_sch_fetch, c_sch_idle;  // scheduler-thread cycles
 };
@@ -102,6 +104,8 @@ struct Params {
     int base_size;
     int budget0;
     int debug_depth;   // > 0: segments at this depth are dropped unsorted (profiling only)
+    uint64_t *leaves;  // queued leaves: begin << 14 | (size - 1) << 1 | in-B
+    unsigned long long leaf_cap;
 };
 
 // ---- key traits ----------------------------------------------------------------------

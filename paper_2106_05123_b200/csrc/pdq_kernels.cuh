@@ -24,6 +24,10 @@
 namespace pdq {
 
 constexpr int CHUNK = 8;                // tiles per ring task (one claim + one descriptor read + one retire)
+#ifndef PDQ_NST
+#define PDQ_NST 1
+#endif
+constexpr int NST = PDQ_NST;            // TMA stages: tile loads run up to NST tiles ahead of compute
 constexpr int RADIX_BITS = 4;
 constexpr int RADIX_DIGITS = 1 << RADIX_BITS;
 constexpr int CNT_BYTES = RADIX_DIGITS * THREADS * 2;  // u16 counters, digit-major
@@ -53,15 +57,18 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, unsigned phase) {
 }
 
 struct Shared {
-    uint64_t bar;            // TMA stage barrier
+    uint64_t bar[NST];       // TMA stage barriers
     uint64_t task;           // current ring task word (0 = exit)
     Seg seg;                 // its descriptor
     uint64_t ntask;          // prefetched next task (0 = none / not yet published)
     Seg nseg;
     unsigned long long npos; // ring position claimed for the next task
     int nstate;              // 0 none, 1 claimed (unpublished), 2 ready, 3 exit
-    int stage_tile;          // tile index whose TMA load is in flight in the stage, or -1
-    int stage_next;          // 1 if the in-flight stage load belongs to the prefetched next task
+    // load cursor (thread 0): tiles issued so far, and which task/tile is the next to load
+    unsigned li;             // loads issued (stage li % NST)
+    unsigned ci;             // tiles consumed by the compute side (mirrors the per-thread counter)
+    int lslot;               // 0: the load cursor is in the current task, 1: in the next task
+    uint32_t ltile;          // next tile index to load within that task
     int wl[WARPS], weq[WARPS];
     long long L, R, lOff, rOff, fL, fE;
     unsigned long long push_pos;
@@ -91,25 +98,39 @@ __device__ __forceinline__ uint32_t mix32(uint64_t x) {
     return (uint32_t)x;
 }
 
-// Dynamic shared memory: the TMA stage, the compaction buffer kc and the base-case scratch kx
-// (keys, then payloads for KV), then the radix counters.  Every pointer is computed
-// arithmetically from the extern shared symbol so the compiler emits LDS/STS, never generic LD/ST.
+// Dynamic shared memory of the persistent sorter: NST TMA stages and the compaction buffer kc
+// (keys, then payloads for KV).  Every pointer is computed arithmetically from the extern shared
+// symbol so the compiler emits LDS/STS, never generic LD/ST.
 template <class U, bool KV>
 struct Bufs {
-    static constexpr int KEY_BYTES = 3 * TILE * (int)sizeof(U);
-    static constexpr int VAL_BYTES = KV ? 3 * TILE * 4 : 0;
-    __device__ __forceinline__ static U *stage() { return reinterpret_cast<U *>(g_dsm); }
-    __device__ __forceinline__ static U *kc() { return reinterpret_cast<U *>(g_dsm) + TILE; }
-    __device__ __forceinline__ static U *kx() { return reinterpret_cast<U *>(g_dsm) + 2 * TILE; }
-    __device__ __forceinline__ static uint32_t *vstage() { return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES); }
-    __device__ __forceinline__ static uint32_t *vc() { return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES) + TILE; }
-    __device__ __forceinline__ static uint32_t *vx() { return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES) + 2 * TILE; }
-    __device__ __forceinline__ static uint16_t *cnt() { return reinterpret_cast<uint16_t *>(g_dsm + KEY_BYTES + VAL_BYTES); }
+    static constexpr int KEY_BYTES = (NST + 1) * TILE * (int)sizeof(U);
+    static constexpr int VAL_BYTES = KV ? (NST + 1) * TILE * 4 : 0;
+    __device__ __forceinline__ static U *stage(int i) { return reinterpret_cast<U *>(g_dsm) + i * TILE; }
+    __device__ __forceinline__ static U *kc() { return reinterpret_cast<U *>(g_dsm) + NST * TILE; }
+    __device__ __forceinline__ static uint32_t *vstage(int i) {
+        return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES) + i * TILE;
+    }
+    __device__ __forceinline__ static uint32_t *vc() { return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES) + NST * TILE; }
     // pivot samples alias kc (free whenever samples are taken)
     __device__ __forceinline__ static uint64_t *samp_k() { return reinterpret_cast<uint64_t *>(kc()); }
     __device__ __forceinline__ static uint32_t *samp_v() {
         return reinterpret_cast<uint32_t *>(reinterpret_cast<unsigned char *>(kc()) + SAMPLES * 8);
     }
+    __host__ __device__ static constexpr int bytes() { return KEY_BYTES + VAL_BYTES; }
+};
+
+// Dynamic shared memory of the base-case kernel: two ping-pong buffers and the radix counters.
+template <class U, bool KV>
+struct BaseBufs {
+    static constexpr int KEY_BYTES = 2 * MAX_BASE * (int)sizeof(U);
+    static constexpr int VAL_BYTES = KV ? 2 * MAX_BASE * 4 : 0;
+    __device__ __forceinline__ static U *kx() { return reinterpret_cast<U *>(g_dsm); }
+    __device__ __forceinline__ static U *kc() { return reinterpret_cast<U *>(g_dsm) + MAX_BASE; }
+    __device__ __forceinline__ static uint32_t *vx() { return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES); }
+    __device__ __forceinline__ static uint32_t *vc() {
+        return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES) + MAX_BASE;
+    }
+    __device__ __forceinline__ static uint16_t *cnt() { return reinterpret_cast<uint16_t *>(g_dsm + KEY_BYTES + VAL_BYTES); }
     __host__ __device__ static constexpr int bytes() { return KEY_BYTES + VAL_BYTES + CNT_BYTES; }
 };
 
@@ -117,6 +138,7 @@ template <class U, bool FLOAT, bool KV>
 struct Sorter {
     using O = Ord<U, FLOAT>;
     using B = Bufs<U, KV>;
+    using BB = BaseBufs<U, KV>;
     static constexpr int VEC = 16 / sizeof(U);
     static constexpr int AL = KV ? 4 : VEC;  // element alignment making both key and payload 16 B aligned
     static constexpr int ELEM_BYTES = sizeof(U) + (KV ? 4 : 0);
@@ -283,29 +305,37 @@ struct Sorter {
                                                    uint32_t vmn) {
         Shared &sh = g_sh;
         const int tid = threadIdx.x;
-        uint32_t *cnt32 = reinterpret_cast<uint32_t *>(B::cnt());
-#pragma unroll
-        for (int i = 0; i < CNT_BYTES / 4 / THREADS; ++i) cnt32[i * THREADS + tid] = 0;
-        csync();
+        csync();  // the previous pass's scatter reads of cnt are done
         const int base = tid * ITEMS;
         U k[ITEMS];
         uint32_t v[ITEMS];
         ld16<U>(ks, base, k);
         if (KV) ld16<uint32_t>(vs, base, v);
-        uint16_t *cnt = B::cnt();
+        uint16_t *cnt = BB::cnt();
         const int nvalid = m - base;  // items r < nvalid are real
+        // per-thread digit counts in registers (8-bit lanes: digits 0-7 in c0, 8-15 in c1) and each
+        // item's rank among this thread's equal digits (4 bits per item in rk): no shared-memory
+        // read-modify-write chains
+        uint64_t c0 = 0, c1 = 0, rk = 0;
 #pragma unroll
         for (int r = 0; r < ITEMS; ++r) {
             const uint32_t d = on_vals ? ((v[r] - vmn) >> shift) & (RADIX_DIGITS - 1)
                                        : (uint32_t)((k[r] - mn) >> shift) & (RADIX_DIGITS - 1);
-            const uint32_t a = d * THREADS + tid;
-            const uint32_t c = cnt[a];
-            if (r < nvalid) cnt[a] = (uint16_t)(c + 1);
+            const uint32_t sh8 = (d & 7u) * 8u;
+            const bool hi = d >= 8;
+            const uint64_t cur = ((hi ? c1 : c0) >> sh8) & 0xFFull;
+            rk |= cur << (4 * r);
+            const uint64_t inc = (r < nvalid) ? (1ull << sh8) : 0ull;
+            c0 += hi ? 0ull : inc;
+            c1 += hi ? inc : 0ull;
         }
+#pragma unroll
+        for (int d = 0; d < RADIX_DIGITS; ++d)
+            cnt[d * THREADS + tid] = (uint16_t)(((d < 8 ? c0 : c1) >> ((d & 7) * 8)) & 0xFFull);
         csync();
         // exclusive scan over the digit-major counter array: thread t owns entries [16t, 16t+16)
         {
-            uint4 *c4 = reinterpret_cast<uint4 *>(B::cnt()) + tid * 2;
+            uint4 *c4 = reinterpret_cast<uint4 *>(BB::cnt()) + tid * 2;
             const uint4 x0 = c4[0], x1 = c4[1];
             uint32_t w0 = x0.x, w1 = x0.y, w2 = x0.z, w3 = x0.w, w4 = x1.x, w5 = x1.y, w6 = x1.z, w7 = x1.w;
             uint32_t run = 0;
@@ -340,10 +370,8 @@ struct Sorter {
         for (int r = 0; r < ITEMS; ++r) {
             const uint32_t d = on_vals ? ((v[r] - vmn) >> shift) & (RADIX_DIGITS - 1)
                                        : (uint32_t)((k[r] - mn) >> shift) & (RADIX_DIGITS - 1);
-            const uint32_t a = d * THREADS + tid;
-            const uint32_t pos = cnt[a];
+            const uint32_t pos = (uint32_t)cnt[d * THREADS + tid] + (uint32_t)((rk >> (4 * r)) & 15u);
             if (r < nvalid) {
-                cnt[a] = (uint16_t)(pos + 1);
                 kd[pos] = k[r];
                 if (KV) vd[pos] = v[r];
             }
@@ -367,8 +395,8 @@ struct Sorter {
         const long long c0 = clock64();
         const U *src = (const U *)(srcB ? P.b_keys : P.a_keys);
         const uint32_t *srcv = srcB ? P.b_vals : P.a_vals;
-        U *bufk[2] = {B::kx(), B::kc()};
-        uint32_t *bufv[2] = {KV ? B::vx() : nullptr, KV ? B::vc() : nullptr};
+        U *bufk[2] = {BB::kx(), BB::kc()};
+        uint32_t *bufv[2] = {KV ? BB::vx() : nullptr, KV ? BB::vc() : nullptr};
         // coalesced load (ordered image), min/max of keys and payload
         U mn = ~(U)0, mx = 0;
         uint32_t vmn = 0xFFFFFFFFu, vmx = 0;
@@ -445,15 +473,48 @@ struct Sorter {
             const uint32_t *fv = bufv[c];
             store_run<uint32_t>(P.a_vals + b, m, [&](int i) { return fv[i]; });
         }
-        __threadfence();
         csync();
         if (tid == 0) {
             sh.s_base++;
             sh.s_bytes += 2ull * ELEM_BYTES * m;
-            finish_keys(P, m);
             sh.s_cyc_base += clock64() - c0;
         }
         csync();
+    }
+
+    // <= 64 keys: warp 0 sorts them in registers (2 per lane, bitonic over shuffles) straight into A.
+    // Padding elements are the maximum (key, payload); a real element equal to the padding is the
+    // same bits, so whichever lands in the first m slots is correct.
+    __device__ static void tiny_sort(const Params &P, bool srcB, int64_t b, int m) {
+        const int tid = threadIdx.x;
+        if (tid < 32) {
+            const U *src = (const U *)(srcB ? P.b_keys : P.a_keys);
+            const uint32_t *srcv = srcB ? P.b_vals : P.a_vals;
+            uint64_t x[2];
+            uint32_t y[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int i = 2 * tid + q;
+                x[q] = i < m ? (uint64_t)O::to(ldcg(src + b + i)) : ~0ull;
+                y[q] = (KV && i < m) ? ldcg(srcv + b + i) : 0xFFFFFFFFu;
+            }
+            warp_bitonic<2>(x, y);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int i = 2 * tid + q;
+                if (i < m) {
+                    ((U *)P.a_keys)[b + i] = O::from((U)x[q]);
+                    if (KV) P.a_vals[b + i] = y[q];
+                }
+            }
+            __threadfence();
+            __syncwarp();
+            if (tid == 0) {
+                g_sh.s_base++;
+                g_sh.s_bytes += 2ull * ELEM_BYTES * m;
+                finish_keys(P, (unsigned long long)m);
+            }
+        }
     }
 
     __device__ static void push_tasks(const Params &P, uint32_t type, uint32_t sid, uint32_t ntiles) {
@@ -540,7 +601,19 @@ struct Sorter {
             return false;
         }
         if (m <= P.base_size) {
-            base_case(P, srcB, b, (int)m);
+            // K7 leaf: tiny ones are sorted right here by one warp, the rest are queued for the
+            // base-case kernel that runs after this one
+            if (m <= 64) {
+                tiny_sort(P, srcB, b, (int)m);
+            } else if (tid == 0) {
+                const unsigned long long pos = atomicAdd(&P.st->leaf_count, 1ull);
+                if (pos < P.leaf_cap)
+                    P.leaves[pos] = (uint64_t)b << 14 | (uint64_t)(m - 1) << 1 | (srcB ? 1u : 0u);
+                else
+                    fail(P, -6);
+                finish_keys(P, (unsigned long long)m);
+            }
+            csync();
             return false;
         }
         // K1: stratified samples (64, or SAMPLES for segments of 2^20+ keys); perturbed strata
@@ -681,9 +754,11 @@ struct Sorter {
         }
     }
 
-    // ---- thread 0: issue the TMA bulk load of tile `tile` of segment `sg` into the stage ---------------
+    // ---- thread 0: issue the TMA bulk load of tile `tile` of segment `sg` into the next stage ----------
     __device__ static void issue_load(const Params &P, const Seg &sg, uint32_t tile) {
         Shared &sh = g_sh;
+        const int st = (int)(sh.li % NST);
+        ++sh.li;
         const int64_t b = sg.begin, e = sg.end;
         const bool srcB = sg.info & I_SRC_B;
         const U *src = (const U *)(srcB ? P.b_keys : P.a_keys);
@@ -695,8 +770,8 @@ struct Sorter {
         const int64_t lo_al = lo & ~(int64_t)(AL - 1);
         int64_t hi_al = (hi + AL - 1) & ~(int64_t)(AL - 1);
         if (hi_al > nfl) hi_al = nfl;
-        U *sk = B::stage();
-        uint32_t *sv = KV ? B::vstage() : nullptr;
+        U *sk = B::stage(st);
+        uint32_t *sv = KV ? B::vstage(st) : nullptr;
         // the array's last < 16 bytes cannot be bulk-copied: scalar loads
         for (int64_t g = (hi_al > lo ? hi_al : lo); g < hi; ++g) {
             sk[g - tbase] = ldcg(src + g);
@@ -705,10 +780,10 @@ struct Sorter {
         const unsigned kb = hi_al > lo_al ? (unsigned)((hi_al - lo_al) * sizeof(U)) : 0u;
         const unsigned vb = (KV && hi_al > lo_al) ? (unsigned)((hi_al - lo_al) * 4) : 0u;
         fence_proxy_async();
-        mbar_expect_tx(&sh.bar, kb + vb);  // the stage barrier's single arrival (+ bytes, maybe 0)
+        mbar_expect_tx(&sh.bar[st], kb + vb);  // the stage barrier's single arrival (+ bytes, maybe 0)
         if (kb) {
-            bulk_g2s(sk + (lo_al - tbase), src + lo_al, kb, &sh.bar);
-            if (KV) bulk_g2s(sv + (lo_al - tbase), srcv + lo_al, vb, &sh.bar);
+            bulk_g2s(sk + (lo_al - tbase), src + lo_al, kb, &sh.bar[st]);
+            if (KV) bulk_g2s(sv + (lo_al - tbase), srcv + lo_al, vb, &sh.bar[st]);
         }
     }
 
@@ -793,7 +868,7 @@ struct Sorter {
     // After the stage is consumed thread 0 starts the next load (next tile of this chunk, or the
     // first tile of the already-claimed next task), so the load overlaps this tile's reservation
     // atomic and stores.
-    __device__ static void part_tile(const Params &P, uint32_t sid, uint32_t tile, unsigned &phase) {
+    __device__ static void part_tile(const Params &P, uint32_t sid, uint32_t tile, unsigned &ci) {
         Shared &sh = g_sh;
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
         const Seg &sg = sh.seg;
@@ -805,13 +880,17 @@ struct Sorter {
         const int64_t tbase = (b / TILE + tile) * (int64_t)TILE;
         const int64_t lo = b > tbase ? b : tbase;
         const int64_t hi = e < tbase + TILE ? e : tbase + TILE;
-        const U *sk = B::stage();
-        const uint32_t *sv = KV ? B::vstage() : nullptr;
+        const int st = (int)(ci % NST);
+        const U *sk = B::stage(st);
+        const uint32_t *sv = KV ? B::vstage(st) : nullptr;
         const U piv = (U)sg.pivot;
         const uint32_t pv = sg.pivot_v;
         const int lo_i = (int)(lo - tbase), hi_i = (int)(hi - tbase);
-        mbar_wait(&sh.bar, phase);
-        phase ^= 1;
+        const long long q0 = clock64();
+        mbar_wait(&sh.bar[st], (ci / NST) & 1u);
+        ++ci;
+        const long long q1 = clock64();
+        if (tid == 0) sh.s_sch_claim += q1 - q0;  // (profiling) stage wait
         unsigned lmask = 0, vmask = 0;
         int eqc = 0;
         if (lo_i == 0 && hi_i == TILE)
@@ -868,7 +947,9 @@ struct Sorter {
             scatter<false>(sk, sv, kc, vc, lmask, vmask, li0, ri0);
         csync();  // stage consumed
         if (tid == 0) {
-            prefetch_next(P, tile);
+            sh.ci = ci;
+            pump_loads(P);
+            const long long q2 = clock64();
             if (packed) {
                 sh.lOff = (long long)(res_lr & 0xFFFFFFFFull);
                 sh.rOff = (long long)(res_lr >> 32);
@@ -876,6 +957,7 @@ struct Sorter {
                 sh.lOff = (long long)res_lr;
                 sh.rOff = (long long)res_r;
             }
+            sh.s_sch_fetch += clock64() - q2;  // (profiling) wait for the reservation atomic
             sh.s_tiles++;
             const bool write_left = !left_mode || srcB;
             sh.s_bytes += (unsigned long long)ELEM_BYTES * (L + R) +
@@ -893,19 +975,34 @@ struct Sorter {
             store_run<U>(dst + e - rOff - R, R, [&](int i) { return kc[L + i]; });
             if (KV) store_run<uint32_t>(dstv + e - rOff - R, R, [&](int i) { return vc[L + i]; });
         }
+        if (tid == 0) sh.s_sch_idle += clock64() - q1;  // (profiling) whole tile after the stage wait
     }
 
-    // thread 0, after tile `tile` of the current task consumed the stage: start the next load
-    __device__ static void prefetch_next(const Params &P, uint32_t tile) {
+    // thread 0: keep NST tile loads in flight ahead of the compute side, walking the current task's
+    // chunk and then, once it is published, the next task's chunk.
+    __device__ static void pump_loads(const Params &P) {
         Shared &sh = g_sh;
-        const uint32_t chunk_end = min(((uint32_t)(sh.task & 0x7FFFFF) + 1) * CHUNK, sh.seg.ntiles);
-        if (tile + 1 < chunk_end) {
-            issue_load(P, sh.seg, tile + 1);
-            return;
+        while (sh.li < sh.ci + NST) {
+            if (sh.lslot == 0) {
+                if (sh.task && ((uint32_t)(sh.task >> 45) & 7u) == T_PART) {
+                    const uint32_t end = min(((uint32_t)(sh.task & 0x7FFFFF) + 1) * CHUNK, sh.seg.ntiles);
+                    if (sh.ltile < end) {
+                        issue_load(P, sh.seg, sh.ltile++);
+                        continue;
+                    }
+                }
+                // the current task has no more tiles: move to the next task
+                if (sh.nstate == 1) poll_next(P);
+                if (sh.nstate != 2) return;
+                sh.lslot = 1;
+                sh.ltile = ((uint32_t)(sh.ntask >> 45) & 7u) == T_PART ? ((uint32_t)sh.ntask & 0x7FFFFF) * CHUNK : 0u;
+            }
+            // load cursor in the next task
+            if (((uint32_t)(sh.ntask >> 45) & 7u) != T_PART) return;
+            const uint32_t end = min(((uint32_t)(sh.ntask & 0x7FFFFF) + 1) * CHUNK, sh.nseg.ntiles);
+            if (sh.ltile >= end) return;
+            issue_load(P, sh.nseg, sh.ltile++);
         }
-        if (sh.nstate == 1) poll_next(P);
-        if (sh.nstate == 2 && ((uint32_t)(sh.ntask >> 45) & 7u) == T_PART)
-            issue_load(P, sh.nseg, ((uint32_t)sh.ntask & 0x7FFFFF) * CHUNK);
     }
 
     // thread 0: non-blocking poll of the claimed next ring position
@@ -947,18 +1044,20 @@ struct Sorter {
                 __nanosleep(ns);
                 if (ns < 1024) ns <<= 1;
             }
-            if (sh.nstate == 2 && ((uint32_t)(sh.ntask >> 45) & 7u) == T_PART)
-                issue_load(P, sh.nseg, ((uint32_t)sh.ntask & 0x7FFFFF) * CHUNK);
         }
         if (sh.nstate == 3) {
             sh.task = 0;
             return;
         }
+        const bool cursor_ahead = sh.lslot == 1;
         sh.task = sh.ntask;
         sh.seg = sh.nseg;
+        sh.lslot = 0;
+        if (!cursor_ahead) sh.ltile = ((uint32_t)(sh.task >> 45) & 7u) == T_PART ? ((uint32_t)sh.task & 0x7FFFFF) * CHUNK : 0u;
         // claim the following position now: its atomic overlaps the whole current task
         sh.npos = atomicAdd(&P.st->q_head, 1ull);
         sh.nstate = 1;
+        pump_loads(P);
     }
 
     __device__ static void fill_tile(const Params &P, const Seg &sg, uint32_t tile) {
@@ -1077,10 +1176,39 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
     if (tid == 0) S::flush_counters(P);
 }
 
+// ---- K7: the base-case kernel: persistent CTAs sort the queued leaves ---------------------------------
+template <class U, bool FLOAT, bool KV>
+__global__ void __launch_bounds__(THREADS, BaseBufs<U, KV>::bytes() <= 45 * 1024 ? 5 : 2) k_base(const __grid_constant__ Params P) {
+    using S = Sorter<U, FLOAT, KV>;
+    Shared &sh = g_sh;
+    const int tid = threadIdx.x;
+    if (ld_volatile_u32(&P.st->reverse)) return;
+    if (tid == 0) S::zero_counters();
+    const unsigned long long count = *(volatile unsigned long long *)&P.st->leaf_count;
+    for (;;) {
+        if (tid == 0) sh.npos = atomicAdd(&P.st->leaf_next, 1ull);
+        csync();
+        const unsigned long long idx = sh.npos;
+        if (idx >= count || idx >= P.leaf_cap) break;
+        const uint64_t lf = P.leaves[idx];
+        S::base_case(P, lf & 1u, (int64_t)(lf >> 14), (int)((lf >> 1) & 0x1FFF) + 1);
+    }
+    csync();
+    if (tid == 0) {
+        atomicAdd(&P.st->c_bytes_base, sh.s_bytes);
+        sh.s_bytes = 0;
+        S::flush_counters(P);
+    }
+}
+
 // ---- K6: the persistent segment-queue sorter --------------------------------------------------------
+#ifndef PDQ_MINB
+#define PDQ_MINB 6
+#endif
 template <class U, bool KV>
 constexpr int sort_min_blocks() {
-    return Bufs<U, KV>::bytes() <= 56 * 1024 ? 4 : (Bufs<U, KV>::bytes() <= 108 * 1024 ? 2 : 1);
+    if (PDQ_MINB > 0 && Bufs<U, KV>::bytes() <= 32 * 1024) return PDQ_MINB;
+    return Bufs<U, KV>::bytes() <= 37 * 1024 ? 6 : (Bufs<U, KV>::bytes() <= 50 * 1024 ? 4 : (Bufs<U, KV>::bytes() <= 74 * 1024 ? 3 : (Bufs<U, KV>::bytes() <= 108 * 1024 ? 2 : 1)));
 }
 
 template <class U, bool FLOAT, bool KV>
@@ -1108,14 +1236,18 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
     }
     if (tid == 0) {
         S::zero_counters();
-        mbar_init(&sh.bar, 1);
+        for (int i = 0; i < NST; ++i) mbar_init(&sh.bar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        sh.li = sh.ci = 0;
+        sh.lslot = 0;
+        sh.ltile = 0;
+        sh.task = 0;
         sh.npos = atomicAdd(&P.st->q_head, 1ull);
         sh.nstate = 1;
         S::advance(P);
     }
     __syncthreads();
-    unsigned phase = 0;
+    unsigned ci = 0;  // tiles consumed (all threads keep the same count)
     long long c_prev = clock64();
     for (;;) {
         const uint64_t w = sh.task;
@@ -1125,7 +1257,7 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
         if (type == T_PART) {
             const uint32_t t0 = ((uint32_t)w & 0x7FFFFF) * CHUNK;
             const uint32_t t1 = min(t0 + CHUNK, sh.seg.ntiles);
-            for (uint32_t t = t0; t < t1; ++t) S::part_tile(P, sid, t, phase);
+            for (uint32_t t = t0; t < t1; ++t) S::part_tile(P, sid, t, ci);
             // retire the chunk: one gpu-scope fence per thread, one counter update per CTA
             __threadfence();
             csync();

@@ -60,6 +60,25 @@ if len(sys.argv) > 4:
         ms = a.elapsed_time(b)
         sch = st['sched_retire'] + st['sched_claim'] + st['sched_fetch'] + st['sched_idle']
         print(f"depth<{d}: {ms:.3f} ms  alg {st['bytes_algorithmic'] / ms / 1e6:.0f} GB/s tiles {st['tiles']} "
-              f"wait {st['cycles_wait'] / (st['cycles_wait'] + st['cycles_work']):.3f} sched: retire "
-              f"{st['sched_retire'] / sch:.3f} claim {st['sched_claim'] / sch:.3f} fetch {st['sched_fetch'] / sch:.3f} "
-              f"idle {st['sched_idle'] / sch:.3f}", flush=True)
+              f"wait {st['cycles_wait'] / (st['cycles_wait'] + st['cycles_work']):.3f} per-tile cycles: stage-wait "
+              f"{st['sched_claim'] / st['tiles']:.0f} tile {st['sched_idle'] / st['tiles']:.0f} (atomic-wait "
+              f"{st['sched_fetch'] / st['tiles']:.0f}) retire/chunk {st['sched_retire'] / max(1, st['tiles'] / 8):.0f}", flush=True)
+
+# kernel split: partition kernel (events from the C ABI) vs whole call
+if len(sys.argv) > 5:
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    ev[0].record()
+    ev[1].record()
+    torch.cuda.synchronize()
+    for r in range(3):
+        x.copy_(src)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        ds.run(x, vals, events=ev)
+        b.record()
+        st = ds.finish()
+    tot = a.elapsed_time(b)
+    ks = ev[0].elapsed_time(ev[1])
+    print(f"split: total {tot:.3f} ms, partition kernel {ks:.3f} ms ({st['bytes_algorithmic'] / ks / 1e6:.0f} GB/s alg), "
+          f"rest (check+init+base) {tot - ks:.3f} ms; base bytes {st['bytes_base'] / 1e9:.2f} GB", flush=True)
