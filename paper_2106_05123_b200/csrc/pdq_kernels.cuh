@@ -28,9 +28,9 @@ constexpr int CHUNK = 8;                // tiles per ring task (one claim + one 
 #define PDQ_NST 1
 #endif
 constexpr int NST = PDQ_NST;            // TMA stages: tile loads run up to NST tiles ahead of compute
-constexpr int RADIX_BITS = 4;
+constexpr int RADIX_BITS = 8;
 constexpr int RADIX_DIGITS = 1 << RADIX_BITS;
-constexpr int CNT_BYTES = RADIX_DIGITS * THREADS * 2;  // u16 counters, digit-major
+constexpr int CNT_BYTES = RADIX_DIGITS * WARPS * 2;  // per-warp u16 digit counters
 
 // compute-warp barrier (named barrier 1): the scheduler warp never joins it
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(THREADS) : "memory"); }
@@ -297,59 +297,69 @@ struct Sorter {
         }
     }
 
-    // One stable counting pass: thread t owns elements [16t, 16t+16) (blocked, so the
-    // thread-major scan of the digit-major u16 counters is the element order) and the counter
-    // column cnt[d][t], which it post-increments again during the scatter.
-    __device__ __noinline__ static void radix_pass(const U *ks, const uint32_t *vs,
-                                                   U *kd, uint32_t *vd, int m, U mn, int shift, bool on_vals,
-                                                   uint32_t vmn) {
+    // One stable 8-bit counting pass.  Warp w owns elements [512w, 512w+512) in 16 rounds of 32
+    // (element 512w + 32j + lane), so (warp, round, lane) is the element order.  Within a round,
+    // __match_any_sync groups equal digits; each group's rank continues the warp's running count
+    // for that digit (per-warp u16 counters in shared memory, updated by the group leader).  One
+    // block-wide scan over (digit, warp) turns the counts into output offsets.
+    __device__ __noinline__ static void radix_pass(const U *ks, const uint32_t *vs, U *kd, uint32_t *vd, int m,
+                                                   U mn, int shift, bool on_vals, uint32_t vmn) {
         Shared &sh = g_sh;
-        const int tid = threadIdx.x;
-        csync();  // the previous pass's scatter reads of cnt are done
-        const int base = tid * ITEMS;
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        uint16_t *wc = BB::cnt() + warp * RADIX_DIGITS;
+        uint32_t *wc32 = reinterpret_cast<uint32_t *>(wc);
+#pragma unroll
+        for (int i = lane; i < RADIX_DIGITS / 2; i += 32) wc32[i] = 0;
+        __syncwarp();
+        const unsigned ltm = lanemask_lt();
+        const int wbase = warp * (32 * ITEMS);
         U k[ITEMS];
         uint32_t v[ITEMS];
-        ld16<U>(ks, base, k);
-        if (KV) ld16<uint32_t>(vs, base, v);
-        uint16_t *cnt = BB::cnt();
-        const int nvalid = m - base;  // items r < nvalid are real
-        // per-thread digit counts in registers (8-bit lanes: digits 0-7 in c0, 8-15 in c1) and each
-        // item's rank among this thread's equal digits (4 bits per item in rk): no shared-memory
-        // read-modify-write chains
-        uint64_t c0 = 0, c1 = 0, rk = 0;
+        uint32_t rd[ITEMS];  // (rank within the warp's digit run) << 8 | digit
+        unsigned pm[ITEMS];  // peers of each round (independent: all matches are issued back to back)
 #pragma unroll
-        for (int r = 0; r < ITEMS; ++r) {
-            const uint32_t d = on_vals ? ((v[r] - vmn) >> shift) & (RADIX_DIGITS - 1)
-                                       : (uint32_t)((k[r] - mn) >> shift) & (RADIX_DIGITS - 1);
-            const uint32_t sh8 = (d & 7u) * 8u;
-            const bool hi = d >= 8;
-            const uint64_t cur = ((hi ? c1 : c0) >> sh8) & 0xFFull;
-            rk |= cur << (4 * r);
-            const uint64_t inc = (r < nvalid) ? (1ull << sh8) : 0ull;
-            c0 += hi ? 0ull : inc;
-            c1 += hi ? inc : 0ull;
+        for (int j = 0; j < ITEMS; ++j) {
+            const int idx = wbase + j * 32 + lane;
+            const bool valid = idx < m;
+            k[j] = valid ? ks[idx] : (U)0;
+            v[j] = (KV && valid) ? vs[idx] : 0u;
+            const uint32_t d = on_vals ? ((v[j] - vmn) >> shift) & (RADIX_DIGITS - 1)
+                                       : (uint32_t)((k[j] - mn) >> shift) & (RADIX_DIGITS - 1);
+            rd[j] = valid ? d : (uint32_t)RADIX_DIGITS;
+            // peers = lanes with the same digit (warp multisplit over the digit's bits: ballots are
+            // full-rate, match.any is not); invalid lanes carry digit 256 and match no valid lane
+            unsigned peers = __ballot_sync(0xffffffffu, valid);
+            peers = valid ? peers : ~peers;
+#pragma unroll
+            for (int bit = 0; bit < RADIX_BITS; ++bit) {
+                const bool on = (d >> bit) & 1u;
+                const unsigned bb = __ballot_sync(0xffffffffu, on);
+                peers &= on ? bb : ~bb;
+            }
+            pm[j] = peers;
         }
+        // sequential part: each round's groups continue the warp's running digit counts
 #pragma unroll
-        for (int d = 0; d < RADIX_DIGITS; ++d)
-            cnt[d * THREADS + tid] = (uint16_t)(((d < 8 ? c0 : c1) >> ((d & 7) * 8)) & 0xFFull);
+        for (int j = 0; j < ITEMS; ++j) {
+            const bool valid = rd[j] < (uint32_t)RADIX_DIGITS;
+            const uint32_t d = rd[j] & (RADIX_DIGITS - 1);
+            const uint32_t before = valid ? (uint32_t)wc[d] : 0u;
+            const uint32_t r = (uint32_t)__popc(pm[j] & ltm);
+            __syncwarp();
+            if (valid && r == 0) wc[d] = (uint16_t)(before + __popc(pm[j]));
+            __syncwarp();
+            rd[j] = ((before + r) << 8) | d;
+        }
         csync();
-        // exclusive scan over the digit-major counter array: thread t owns entries [16t, 16t+16)
+        // digit-major exclusive scan: thread t owns digit t across the warps
         {
-            uint4 *c4 = reinterpret_cast<uint4 *>(BB::cnt()) + tid * 2;
-            const uint4 x0 = c4[0], x1 = c4[1];
-            uint32_t w0 = x0.x, w1 = x0.y, w2 = x0.z, w3 = x0.w, w4 = x1.x, w5 = x1.y, w6 = x1.z, w7 = x1.w;
-            uint32_t run = 0;
-#define PDQ_PFX(wq)                                     \
-    {                                                   \
-        const uint32_t lo = wq & 0xFFFF, hi = wq >> 16; \
-        const uint32_t e0 = run, e1 = run + lo;         \
-        run = e1 + hi;                                  \
-        wq = e0 | (e1 << 16);                           \
-    }
-            PDQ_PFX(w0) PDQ_PFX(w1) PDQ_PFX(w2) PDQ_PFX(w3) PDQ_PFX(w4) PDQ_PFX(w5) PDQ_PFX(w6) PDQ_PFX(w7)
-#undef PDQ_PFX
-            const int lane = tid & 31, warp = tid >> 5;
-            uint32_t inc = run;
+            uint32_t c[WARPS], tot = 0;
+#pragma unroll
+            for (int w = 0; w < WARPS; ++w) {
+                c[w] = BB::cnt()[w * RADIX_DIGITS + tid];
+                tot += c[w];
+            }
+            uint32_t inc = tot;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
@@ -357,23 +367,22 @@ struct Sorter {
             }
             if (lane == 31) sh.scan[warp] = inc;
             csync();
-            uint32_t wpre = 0;
+            uint32_t run = inc - tot;
 #pragma unroll
-            for (int q = 0; q < WARPS; ++q) wpre += (q < warp) ? sh.scan[q] : 0u;
-            const uint32_t pre = wpre + inc - run;
-            const uint32_t pre2 = pre | (pre << 16);
-            c4[0] = make_uint4(w0 + pre2, w1 + pre2, w2 + pre2, w3 + pre2);
-            c4[1] = make_uint4(w4 + pre2, w5 + pre2, w6 + pre2, w7 + pre2);
+            for (int q = 0; q < WARPS; ++q) run += (q < warp) ? sh.scan[q] : 0u;
+#pragma unroll
+            for (int w = 0; w < WARPS; ++w) {
+                BB::cnt()[w * RADIX_DIGITS + tid] = (uint16_t)run;
+                run += c[w];
+            }
         }
         csync();
 #pragma unroll
-        for (int r = 0; r < ITEMS; ++r) {
-            const uint32_t d = on_vals ? ((v[r] - vmn) >> shift) & (RADIX_DIGITS - 1)
-                                       : (uint32_t)((k[r] - mn) >> shift) & (RADIX_DIGITS - 1);
-            const uint32_t pos = (uint32_t)cnt[d * THREADS + tid] + (uint32_t)((rk >> (4 * r)) & 15u);
-            if (r < nvalid) {
-                kd[pos] = k[r];
-                if (KV) vd[pos] = v[r];
+        for (int j = 0; j < ITEMS; ++j) {
+            if (wbase + j * 32 + lane < m) {
+                const uint32_t pos = (uint32_t)wc[rd[j] & 0xFFu] + (rd[j] >> 8);
+                kd[pos] = k[j];
+                if (KV) vd[pos] = v[j];
             }
         }
         csync();
