@@ -143,6 +143,16 @@ struct Sorter {
     static constexpr int AL = KV ? 4 : VEC;  // element alignment making both key and payload 16 B aligned
     static constexpr int ELEM_BYTES = sizeof(U) + (KV ? 4 : 0);
     using SU = typename std::conditional<sizeof(U) == 4, int32_t, int64_t>::type;
+    static constexpr int NBYTES = (int)sizeof(U) + (KV ? 4 : 0);  // radix digits of an element
+
+    // byte `rb` (0 = most significant) of the element's ordered image (key bytes, then payload)
+    __device__ __forceinline__ static uint32_t rdigit(U k, uint32_t v, int rb) {
+        if (rb < (int)sizeof(U)) return (uint32_t)(O::to(k) >> (8 * ((int)sizeof(U) - 1 - rb))) & 255u;
+        return (v >> (8 * (3 - (rb - (int)sizeof(U))))) & 255u;
+    }
+    __device__ __forceinline__ static bool tile_task(uint32_t type) {
+        return type == T_PART || type == T_RHIST || type == T_RSCAT;
+    }
 
     // strict order on raw key bits (+ payload): ints compare signed, floats by total order
     __device__ __forceinline__ static bool lt_raw(U a, uint32_t va, U b, uint32_t vb) {
@@ -585,7 +595,7 @@ struct Sorter {
     // Returns true iff the reusable descriptor `reuse_sid` was consumed.
     __device__ static bool spawn(const Params &P, int64_t b, int64_t e, bool srcB,
                                  bool has_lb, uint64_t lb, uint32_t lbv, int budget, int depth, bool perturb,
-                                 int reuse_sid) {
+                                 int reuse_sid, int rbyte) {
         Shared &sh = g_sh;
         const int tid = threadIdx.x;
         const int64_t m = e - b;
@@ -624,6 +634,15 @@ struct Sorter {
             }
             csync();
             return false;
+        }
+        // K5: the bad-partition budget is spent (driver.py:209-213): split the segment on its next
+        // radix digit instead of partitioning it again.  If the histogram pool is exhausted the
+        // segment keeps quicksorting with perturbed samples.
+        if (budget <= 0 && rbyte < NBYTES) {
+            if (tid == 0) sh.s_fallback++;
+            const int r = radix_start(P, b, e, srcB, rbyte, depth, reuse_sid);
+            if (r >= 0) return r > 0;
+            perturb = true;
         }
         // K1: stratified samples (64, or SAMPLES for segments of 2^20+ keys); perturbed strata
         // after a bad partition.  The median of the sorted sample is the pivot.
@@ -682,7 +701,6 @@ struct Sorter {
             uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
             sh.new_sid = sid;
             sh.s_bytes += (unsigned long long)SAMPLES * ELEM_BYTES;
-            if (!left && budget <= 0) sh.s_fallback++;
             if (sid >= P.seg_cap) {
                 fail(P, -6);
             } else {
@@ -698,6 +716,7 @@ struct Sorter {
                           (perturb ? I_PERTURB : 0) | (dup_heavy ? I_COUNT_EQ : 0);
                 s->budget = budget > 0 ? budget : 0;
                 s->depth = depth;
+                s->rbyte = (unsigned)rbyte;
                 s->cnt_left = 0;
                 s->cnt_right = 0;
                 s->cnt_eq = 0;
@@ -745,9 +764,9 @@ struct Sorter {
             const int nb = sg.budget - (bad ? 1 : 0);
             const bool perturb = bad && P.use_break;
             bool used = spawn(P, b, b + L, dstB, sg.info & I_HAS_LB, sg.lb, sg.lb_v, nb, sg.depth + 1,
-                              perturb, (int)sid);
+                              perturb, (int)sid, (int)sg.rbyte);
             spawn(P, b + L, e, dstB, true, piv_ord, sg.pivot_v, nb, sg.depth + 1, perturb,
-                  used ? -1 : (int)sid);
+                  used ? -1 : (int)sid, (int)sg.rbyte);
         } else {
             if (tid == 0) sh.s_part_left++;
             bool used = false;
@@ -759,7 +778,234 @@ struct Sorter {
                 used = fill_final(P, b, b + L, piv_ord, sg.pivot_v, (int)sid);
             }
             spawn(P, b + L, e, dstB, true, piv_ord, sg.pivot_v, sg.budget, sg.depth + 1, false,
-                  used ? -1 : (int)sid);
+                  used ? -1 : (int)sid, (int)sg.rbyte);
+        }
+    }
+
+    // ---- K5: MSD radix split (the fallback) -----------------------------------------------------------
+    // Phase 1 (T_RHIST tiles): 256-bin histogram of digit `rbyte`.  Phase 2 (T_RSCAT tiles): every
+    // tile reserves its per-bucket runs with one atomic per non-empty bucket and scatters into the
+    // other buffer.  Buckets then resume quicksort with a fresh budget and the next digit, so a
+    // sustained adversary costs at most one split per digit along any path.
+    // Returns 1 if `reuse_sid` was consumed, 0 if not, -1 if no histogram slot was free.
+    __device__ static int radix_start(const Params &P, int64_t b, int64_t e, bool srcB, int rbyte, int depth,
+                                      int reuse_sid) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x;
+        if (tid == 0) sh.new_sid = atomicAdd(&P.st->hpool_alloc, 1u);
+        csync();
+        const uint32_t hs = sh.new_sid;
+        csync();
+        if (hs >= P.hpool_cap) return -1;
+        uint32_t *h = P.hpool + (size_t)hs * HSLOT;
+        for (int i = tid; i < HSLOT; i += THREADS) h[i] = 0u;
+        __threadfence();
+        csync();
+        const uint32_t ntiles = (uint32_t)((e - 1) / TILE - b / TILE + 1);
+        const uint32_t nchunks = (ntiles + CHUNK - 1) / CHUNK;
+        if (tid == 0) {
+            const uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
+            sh.new_sid = sid;
+            if (sid >= P.seg_cap) {
+                fail(P, -6);
+            } else {
+                Seg *s = &P.segs[sid];
+                s->begin = b;
+                s->end = e;
+                s->info = I_RADIX | (srcB ? I_SRC_B : 0u);
+                s->rbyte = (unsigned)rbyte;
+                s->hidx = hs;
+                s->ntiles = ntiles;
+                s->depth = depth;
+                s->budget = 0;
+                s->tiles_done = 0;
+                __threadfence();
+                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)nchunks);
+            }
+        }
+        csync();
+        if (sh.new_sid < P.seg_cap) push_tasks(P, T_RHIST, sh.new_sid, nchunks);
+        csync();
+        return reuse_sid >= 0 ? 1 : 0;
+    }
+
+    __device__ static void rhist_tile(const Params &P, uint32_t tile, unsigned &ci) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x;
+        const Seg &sg = sh.seg;
+        const int64_t tbase = (sg.begin / TILE + tile) * (int64_t)TILE;
+        const int lo_i = (int)((sg.begin > tbase ? sg.begin : tbase) - tbase);
+        const int hi_i = (int)((sg.end < tbase + TILE ? sg.end : tbase + TILE) - tbase);
+        const int st = (int)(ci % NST);
+        mbar_wait(&sh.bar[st], (ci / NST) & 1u);
+        ++ci;
+        uint32_t *hist = reinterpret_cast<uint32_t *>(B::kc());
+        csync();  // the previous tile may still be reading kc
+        hist[tid] = 0u;
+        csync();
+        const U *sk = B::stage(st);
+        const uint32_t *sv = KV ? B::vstage(st) : nullptr;
+        const int rb = (int)sg.rbyte;
+        for (int i = lo_i + tid; i < hi_i; i += THREADS) atomicAdd(&hist[rdigit(sk[i], KV ? sv[i] : 0u, rb)], 1u);
+        csync();  // stage consumed
+        if (tid == 0) {
+            sh.ci = ci;
+            pump_loads(P);
+            sh.s_tiles++;
+            sh.s_bytes += (unsigned long long)ELEM_BYTES * (hi_i - lo_i);
+        }
+        const uint32_t c = hist[tid];
+        if (c) atomicAdd(&P.hpool[(size_t)sg.hidx * HSLOT + 256 + tid], c);
+    }
+
+    __device__ static void rscat_tile(const Params &P, uint32_t tile, unsigned &ci) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x;
+        const Seg &sg = sh.seg;
+        const int64_t tbase = (sg.begin / TILE + tile) * (int64_t)TILE;
+        const int lo_i = (int)((sg.begin > tbase ? sg.begin : tbase) - tbase);
+        const int hi_i = (int)((sg.end < tbase + TILE ? sg.end : tbase + TILE) - tbase);
+        const bool srcB = sg.info & I_SRC_B;
+        U *dst = (U *)(srcB ? P.a_keys : P.b_keys);
+        uint32_t *dstv = srcB ? P.a_vals : P.b_vals;
+        const int st = (int)(ci % NST);
+        mbar_wait(&sh.bar[st], (ci / NST) & 1u);
+        ++ci;
+        uint32_t *hist = reinterpret_cast<uint32_t *>(B::kc());
+        csync();  // the previous tile may still be reading kc
+        hist[tid] = 0u;
+        csync();
+        const U *sk = B::stage(st);
+        const uint32_t *sv = KV ? B::vstage(st) : nullptr;
+        const int rb = (int)sg.rbyte;
+        U k[ITEMS];
+        uint32_t v[ITEMS], pk[ITEMS];
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+            const int i = r * THREADS + tid;
+            const bool valid = i >= lo_i && i < hi_i;
+            k[r] = sk[i];
+            v[r] = KV ? sv[i] : 0u;
+            const uint32_t d = rdigit(k[r], v[r], rb);
+            pk[r] = valid ? (d | atomicAdd(&hist[d], 1u) << 8) : 0xFFFFFFFFu;  // rank within the tile
+        }
+        csync();  // stage consumed, tile histogram complete
+        if (tid == 0) {
+            sh.ci = ci;
+            pump_loads(P);
+            sh.s_tiles++;
+            sh.s_bytes += 2ull * ELEM_BYTES * (hi_i - lo_i);
+        }
+        const uint32_t c = hist[tid];
+        const uint32_t base = c ? atomicAdd(&P.hpool[(size_t)sg.hidx * HSLOT + tid], c) : 0u;
+        csync();
+        hist[tid] = base;
+        csync();
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+            if (pk[r] != 0xFFFFFFFFu) {
+                const int64_t pos = sg.begin + hist[pk[r] & 255u] + (pk[r] >> 8);
+                dst[pos] = k[r];
+                if (KV) dstv[pos] = v[r];
+            }
+        }
+        csync();
+    }
+
+    // block-wide exclusive scan of one u32 per thread (THREADS == 256 == radix bins)
+    __device__ static uint32_t block_excl_scan(uint32_t x) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        uint32_t inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        csync();
+        if (lane == 31) sh.scan[warp] = inc;
+        csync();
+        uint32_t pre = inc - x;
+#pragma unroll
+        for (int q = 0; q < WARPS; ++q) pre += (q < warp) ? sh.scan[q] : 0u;
+        return pre;
+    }
+
+    // Every key of [b, e) (in buffer srcB) is bitwise identical: make A hold it.
+    __device__ static void finish_constant(const Params &P, int64_t b, int64_t e, bool srcB) {
+        if (srcB) {
+            const U k0 = ldcg((const U *)P.b_keys + b);
+            const uint32_t v0 = KV ? ldcg(P.b_vals + b) : 0u;
+            fill_final(P, b, e, (uint64_t)O::to(k0), v0, -1);
+        } else {
+            if (threadIdx.x == 0) finish_keys(P, (unsigned long long)(e - b));
+            csync();
+        }
+    }
+
+    __device__ __noinline__ static void finalize_rhist(const Params &P, const Seg &sg, uint32_t sid) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x;
+        const int64_t b = sg.begin, e = sg.end, m = e - b;
+        uint32_t *h = P.hpool + (size_t)sg.hidx * HSLOT;
+        const uint32_t c = __ldcg(&h[256 + tid]);
+        const uint32_t nchunks = (sg.ntiles + CHUNK - 1) / CHUNK;
+        if (csync_or((int64_t)c == m)) {
+            // one bucket holds everything: this digit carries no information
+            if ((int)sg.rbyte + 1 >= NBYTES) {
+                finish_constant(P, b, e, sg.info & I_SRC_B);
+                return;
+            }
+            h[256 + tid] = 0u;
+            __threadfence();
+            csync();
+            if (tid == 0) {
+                Seg *s = &P.segs[sid];
+                s->rbyte = sg.rbyte + 1;
+                s->tiles_done = 0;
+                __threadfence();
+                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)nchunks);
+            }
+            csync();
+            push_tasks(P, T_RHIST, sid, nchunks);
+            csync();
+            return;
+        }
+        h[tid] = block_excl_scan(c);  // bucket cursors (relative to begin)
+        __threadfence();
+        csync();
+        if (tid == 0) {
+            Seg *s = &P.segs[sid];
+            s->tiles_done = 0;
+            __threadfence();
+            sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)nchunks);
+        }
+        csync();
+        push_tasks(P, T_RSCAT, sid, nchunks);
+        csync();
+    }
+
+    __device__ __noinline__ static void finalize_rscat(const Params &P, const Seg &sg, uint32_t sid) {
+        const int tid = threadIdx.x;
+        const int64_t b = sg.begin;
+        const bool dstB = !(sg.info & I_SRC_B);
+        // bucket counts and start offsets stay in the parent's histogram slot (children take new
+        // slots); shared memory cannot hold them because spawned children sample into kc
+        const uint32_t *h = P.hpool + (size_t)sg.hidx * HSLOT;
+        if (tid == 0) g_sh.s_part_right++;
+        const int nrb = (int)sg.rbyte + 1;
+        bool reused = false;
+        for (int d = 0; d < 256; ++d) {
+            const uint32_t cd = __ldcg(&h[256 + d]);
+            if (!cd) continue;
+            const int64_t cb = b + (__ldcg(&h[d]) - cd);  // the cursor advanced by exactly the count
+            if (nrb >= NBYTES) {
+                finish_constant(P, cb, cb + cd, dstB);  // every digit matched: identical elements
+            } else {
+                const int budget = 63 - __clzll((long long)cd);  // a fresh budget for the bucket
+                reused |= spawn(P, cb, cb + cd, dstB, false, 0, 0, budget, sg.depth + 1, false,
+                                reused ? -1 : (int)sid, nrb);
+            }
         }
     }
 
@@ -993,7 +1239,7 @@ struct Sorter {
         Shared &sh = g_sh;
         while (sh.li < sh.ci + NST) {
             if (sh.lslot == 0) {
-                if (sh.task && ((uint32_t)(sh.task >> 45) & 7u) == T_PART) {
+                if (sh.task && tile_task((uint32_t)(sh.task >> 45) & 7u)) {
                     const uint32_t end = min(((uint32_t)(sh.task & 0x7FFFFF) + 1) * CHUNK, sh.seg.ntiles);
                     if (sh.ltile < end) {
                         issue_load(P, sh.seg, sh.ltile++);
@@ -1004,10 +1250,10 @@ struct Sorter {
                 if (sh.nstate == 1) poll_next(P);
                 if (sh.nstate != 2) return;
                 sh.lslot = 1;
-                sh.ltile = ((uint32_t)(sh.ntask >> 45) & 7u) == T_PART ? ((uint32_t)sh.ntask & 0x7FFFFF) * CHUNK : 0u;
+                sh.ltile = tile_task((uint32_t)(sh.ntask >> 45) & 7u) ? ((uint32_t)sh.ntask & 0x7FFFFF) * CHUNK : 0u;
             }
             // load cursor in the next task
-            if (((uint32_t)(sh.ntask >> 45) & 7u) != T_PART) return;
+            if (!tile_task((uint32_t)(sh.ntask >> 45) & 7u)) return;
             const uint32_t end = min(((uint32_t)(sh.ntask & 0x7FFFFF) + 1) * CHUNK, sh.nseg.ntiles);
             if (sh.ltile >= end) return;
             issue_load(P, sh.nseg, sh.ltile++);
@@ -1062,7 +1308,7 @@ struct Sorter {
         sh.task = sh.ntask;
         sh.seg = sh.nseg;
         sh.lslot = 0;
-        if (!cursor_ahead) sh.ltile = ((uint32_t)(sh.task >> 45) & 7u) == T_PART ? ((uint32_t)sh.task & 0x7FFFFF) * CHUNK : 0u;
+        if (!cursor_ahead) sh.ltile = tile_task((uint32_t)(sh.task >> 45) & 7u) ? ((uint32_t)sh.task & 0x7FFFFF) * CHUNK : 0u;
         // claim the following position now: its atomic overlaps the whole current task
         sh.npos = atomicAdd(&P.st->q_head, 1ull);
         sh.nstate = 1;
@@ -1179,7 +1425,7 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
     if (s_action == 0) {
         int budget = P.budget0;
         if (budget < 0) budget = 63 - __clzll((long long)P.n);  // driver.py:263: n.bit_length() - 1
-        S::spawn(P, 0, P.n, false, false, 0, 0, budget, 0, false, -1);
+        S::spawn(P, 0, P.n, false, false, 0, 0, budget, 0, false, -1, 0);
     }
     __syncthreads();
     if (tid == 0) S::flush_counters(P);
@@ -1263,10 +1509,17 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
         if (!w) break;
         const uint32_t type = (uint32_t)(w >> 45) & 7u;
         const uint32_t sid = (uint32_t)(w >> 23) & 0x3FFFFF;
-        if (type == T_PART) {
+        if (S::tile_task(type)) {
             const uint32_t t0 = ((uint32_t)w & 0x7FFFFF) * CHUNK;
             const uint32_t t1 = min(t0 + CHUNK, sh.seg.ntiles);
-            for (uint32_t t = t0; t < t1; ++t) S::part_tile(P, sid, t, ci);
+            for (uint32_t t = t0; t < t1; ++t) {
+                if (type == T_PART)
+                    S::part_tile(P, sid, t, ci);
+                else if (type == T_RHIST)
+                    S::rhist_tile(P, t, ci);
+                else
+                    S::rscat_tile(P, t, ci);
+            }
             // retire the chunk: one gpu-scope fence per thread, one counter update per CTA
             __threadfence();
             csync();
@@ -1279,7 +1532,12 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
             csync();
             if (sh.last) {
                 __threadfence();
-                S::finalize_part(P, sh.seg, sid);
+                if (type == T_PART)
+                    S::finalize_part(P, sh.seg, sid);
+                else if (type == T_RHIST)
+                    S::finalize_rhist(P, sh.seg, sid);
+                else
+                    S::finalize_rscat(P, sh.seg, sid);
             }
         } else {  // T_FILL
             S::fill_tile(P, sh.seg, (uint32_t)w & 0x7FFFFF);

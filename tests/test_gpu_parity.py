@@ -177,13 +177,38 @@ def test_toggle_soundness():
             assert same_bytes(got, np.sort(keys)), (bits, n)
 
 
-def test_forced_fallback_budget_zero():
-    # bad_budget=0: every big segment starts with an exhausted budget (K5 path)
+@pytest.mark.parametrize("dtype", DTYPES + ["kv"], ids=lambda d: d if isinstance(d, str) else np.dtype(d).name)
+def test_forced_fallback_budget_zero(dtype):
+    # bad_budget=0: the root starts with an exhausted budget, so it takes the K5 radix split
+    # (driver.py:209-213 analogue); buckets resume quicksort with a fresh budget
     rng = np.random.default_rng(5)
-    keys = rng.integers(-(2**31), 2**31, 300000, dtype=np.int64).astype(np.int32)
-    got, _, stats = gpu_sort(keys, config=SortConfig(bad_budget=0))
+    for n in (5000, 300000, 1 << 22):
+        if dtype == "kv":
+            keys = rng.integers(0, 50, n).astype(np.int64)
+            vals = rng.integers(0, 2**32, n, dtype=np.uint32)
+        elif np.dtype(dtype).kind == "f":
+            keys, vals = rng.standard_normal(n).astype(dtype), None
+        else:
+            info = np.iinfo(dtype)
+            keys, vals = rng.integers(info.min, info.max, n, dtype=dtype), None
+        got_k, got_v, stats = gpu_sort(keys, vals, config=SortConfig(bad_budget=0))
+        exp_k, exp_v = workloads.expected(keys, vals)
+        assert same_bytes(got_k, exp_k) and (vals is None or same_bytes(got_v, exp_v)), n
+        assert stats["radix_fallbacks"] >= 1
+
+
+def test_bad_shift_one_exhausts_budgets_deep_in_the_tree():
+    # bad_partition_shift=1 calls almost every split bad (min side < half), so budgets run out
+    # along many paths and the radix split fires repeatedly at depth, with pattern breaking on
+    rng = np.random.default_rng(6)
+    for dtype in (np.int32, np.int64):
+        keys = rng.integers(-(2**31), 2**31, 1 << 21).astype(dtype)
+        got, _, stats = gpu_sort(keys, config=SortConfig(bad_partition_shift=1, bad_budget=4))
+        assert same_bytes(got, np.sort(keys))
+        assert stats["bad_partitions"] > 10 and stats["radix_fallbacks"] >= 2, stats
+    keys = rng.integers(0, 1000, 1 << 21).astype(np.int32)
+    got, _, stats = gpu_sort(keys, config=SortConfig(bad_partition_shift=1, bad_budget=2, use_break_patterns=False))
     assert same_bytes(got, np.sort(keys))
-    assert stats["radix_fallbacks"] >= 1
 
 
 def test_low_cardinality_uses_partition_left():
