@@ -59,9 +59,8 @@ namespace {
 constexpr int MIN_BASE = 1024;
 
 struct Layout {
-    size_t b_keys, b_vals, state, segs, ring, leaves, hpool, total;
+    size_t b_keys, b_vals, state, segs, ring, leaves, total;
     uint64_t leaf_cap;
-    uint32_t hpool_cap;
     uint32_t seg_cap;
     int log_q;
 };
@@ -105,10 +104,6 @@ Layout layout(int dtype, int has_payload, int64_t n) {
     L.leaf_cap = (uint64_t)n / 64 + 16;
     L.leaves = off;
     off += a256((size_t)L.leaf_cap * 8);
-    // K5 radix histograms (one slot per concurrently splitting segment; rare)
-    L.hpool_cap = (uint32_t)(256 + (uint64_t)n / (1 << 20));
-    L.hpool = off;
-    off += a256((size_t)L.hpool_cap * HSLOT * 4);
     L.total = off;
     return L;
 }
@@ -245,8 +240,7 @@ extern "C" int pdq_sort_ex(void *keys, int dtype, uint32_t *payload, int64_t n, 
     P.debug_depth = cfg.reserved[0];
     P.leaves = (uint64_t *)(ws + L.leaves);
     P.leaf_cap = L.leaf_cap;
-    P.hpool = (uint32_t *)(ws + L.hpool);
-    P.hpool_cap = L.hpool_cap;
+
 
     const bool kv = payload != nullptr;
     switch (dtype) {

@@ -26,7 +26,7 @@ constexpr int64_t INLINE_FILL = 16 * TILE;  // fills up to this size run inline 
 // ---- task ring --------------------------------------------------------------------
 // A task is one 64-bit word carrying its own round tag, so publishing it is a
 // single store:  [63:48] round tag | [47:45] type | [44:23] segment | [22:0] tile.
-enum : uint32_t { T_PART = 1, T_FILL = 2, T_RHIST = 3, T_RSCAT = 4 };
+enum : uint32_t { T_PART = 1, T_FILL = 2 };
 __host__ __device__ inline uint64_t task_word(uint64_t pos, int log_q, uint32_t type, uint32_t seg,
                                               uint32_t tile) {
     return ((pos >> log_q) & 0xFFFFull) << 48 | (uint64_t)(type & 7) << 45 |
@@ -43,7 +43,8 @@ enum : uint32_t {
     I_HAS_LB = 1u << 2,   // `lb` is a valid lower bound = the reference's predecessor (driver.py:222)
     I_PERTURB = 1u << 3,  // sample positions perturbed (pattern breaking, driver.py:239-243)
     I_COUNT_EQ = 1u << 4, // the sample's low end repeats the pivot: count keys equal to it
-    I_RADIX = 1u << 5,    // K5 fallback: the segment is split on one radix digit (MSD byte `rbyte`)
+    I_RADIX = 1u << 5,    // K5 fallback: radix exchange on composite bit `rbit` (threshold pivot)
+    I_HAS_UB = 1u << 6,   // `ub` is a valid exclusive upper bound
 };
 
 struct __align__(128) Seg {
@@ -59,10 +60,11 @@ struct __align__(128) Seg {
     unsigned long long cnt_right;  //          keys reserved on the right side
     unsigned long long cnt_eq;     //          keys bitwise equal to the pivot (RIGHT mode)
     unsigned int tiles_done;
-    unsigned int rbyte;   // next radix digit (byte index from the most significant) for a fallback
-    uint32_t hidx;        // radix histogram slot (I_RADIX segments)
+    unsigned int rbit;    // I_RADIX: the composite bit this split decides (0 = most significant)
+    uint32_t ub_v;
     uint32_t pad0;
-    uint64_t pad1[2];
+    uint64_t ub;          // exclusive upper bound (ordered), valid iff I_HAS_UB
+    uint64_t pad1;
 };
 static_assert(sizeof(Seg) == 128, "Seg is one 128-byte line");
 
@@ -78,7 +80,7 @@ struct __align__(128) State {
     int status;
     unsigned int check_bits;       // K4: 1 descent seen, 2 ascent seen
     unsigned int reverse;          // K4 decided the input is non-increasing
-    unsigned int hpool_alloc;      // radix histogram slots handed out
+    unsigned int pad_c;
     unsigned long long pad_d[12];
     // counters (pdq_stats order)
     unsigned long long leaf_count;  // queued base-case segments (K7 kernel input)
@@ -109,10 +111,7 @@ struct Params {
     int debug_depth;   // > 0: segments at this depth are dropped unsorted (profiling only)
     uint64_t *leaves;  // queued leaves: begin << 14 | (size - 1) << 1 | in-B
     unsigned long long leaf_cap;
-    uint32_t *hpool;   // radix histograms: HSLOT u32 per slot (256 cursors, 256 counts)
-    uint32_t hpool_cap;
 };
-constexpr int HSLOT = 512;
 
 // ---- key traits ----------------------------------------------------------------------
 template <class U, bool FLOAT>

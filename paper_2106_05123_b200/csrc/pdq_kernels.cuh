@@ -143,16 +143,18 @@ struct Sorter {
     static constexpr int AL = KV ? 4 : VEC;  // element alignment making both key and payload 16 B aligned
     static constexpr int ELEM_BYTES = sizeof(U) + (KV ? 4 : 0);
     using SU = typename std::conditional<sizeof(U) == 4, int32_t, int64_t>::type;
-    static constexpr int NBYTES = (int)sizeof(U) + (KV ? 4 : 0);  // radix digits of an element
+    
+    static constexpr int KBITS = 8 * (int)sizeof(U);
+    static constexpr int NBITS = KBITS + (KV ? 32 : 0);  // bits of the (ordered key, payload) composite
+    __device__ __forceinline__ static bool tile_task(uint32_t type) { return type == T_PART; }
 
-    // byte `rb` (0 = most significant) of the element's ordered image (key bytes, then payload)
-    __device__ __forceinline__ static uint32_t rdigit(U k, uint32_t v, int rb) {
-        if (rb < (int)sizeof(U)) return (uint32_t)(O::to(k) >> (8 * ((int)sizeof(U) - 1 - rb))) & 255u;
-        return (v >> (8 * (3 - (rb - (int)sizeof(U))))) & 255u;
-    }
-    __device__ __forceinline__ static bool tile_task(uint32_t type) {
-        return type == T_PART || type == T_RHIST || type == T_RSCAT;
-    }
+    // Bounds known for a segment: every element e satisfies lb <= e (has_lb) and e < ub (has_ub),
+    // in the (ordered key, payload) order.  lb is the reference's predecessor (driver.py:222).
+    struct Bnd {
+        uint64_t lb, ub;
+        uint32_t lbv, ubv;
+        bool has_lb, has_ub;
+    };
 
     // strict order on raw key bits (+ payload): ints compare signed, floats by total order
     __device__ __forceinline__ static bool lt_raw(U a, uint32_t va, U b, uint32_t vb) {
@@ -323,21 +325,17 @@ struct Sorter {
         __syncwarp();
         const unsigned ltm = lanemask_lt();
         const int wbase = warp * (32 * ITEMS);
-        U k[ITEMS];
-        uint32_t v[ITEMS];
-        uint32_t rd[ITEMS];  // (rank within the warp's digit run) << 8 | digit
-        unsigned pm[ITEMS];  // peers of each round (independent: all matches are issued back to back)
+        uint32_t rd[ITEMS];  // (rank within the warp's digit run) << 8 | digit; keys are re-read later
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) {
             const int idx = wbase + j * 32 + lane;
             const bool valid = idx < m;
-            k[j] = valid ? ks[idx] : (U)0;
-            v[j] = (KV && valid) ? vs[idx] : 0u;
-            const uint32_t d = on_vals ? ((v[j] - vmn) >> shift) & (RADIX_DIGITS - 1)
-                                       : (uint32_t)((k[j] - mn) >> shift) & (RADIX_DIGITS - 1);
-            rd[j] = valid ? d : (uint32_t)RADIX_DIGITS;
+            const U kk = valid ? ks[idx] : (U)0;
+            const uint32_t vv = (KV && valid) ? vs[idx] : 0u;
+            const uint32_t d = on_vals ? ((vv - vmn) >> shift) & (RADIX_DIGITS - 1)
+                                       : (uint32_t)((kk - mn) >> shift) & (RADIX_DIGITS - 1);
             // peers = lanes with the same digit (warp multisplit over the digit's bits: ballots are
-            // full-rate, match.any is not); invalid lanes carry digit 256 and match no valid lane
+            // full-rate, match.any is not); invalid lanes match no valid lane
             unsigned peers = __ballot_sync(0xffffffffu, valid);
             peers = valid ? peers : ~peers;
 #pragma unroll
@@ -346,17 +344,11 @@ struct Sorter {
                 const unsigned bb = __ballot_sync(0xffffffffu, on);
                 peers &= on ? bb : ~bb;
             }
-            pm[j] = peers;
-        }
-        // sequential part: each round's groups continue the warp's running digit counts
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-            const bool valid = rd[j] < (uint32_t)RADIX_DIGITS;
-            const uint32_t d = rd[j] & (RADIX_DIGITS - 1);
+            // the group continues the warp's running count for digit d; its leader advances it
             const uint32_t before = valid ? (uint32_t)wc[d] : 0u;
-            const uint32_t r = (uint32_t)__popc(pm[j] & ltm);
+            const uint32_t r = (uint32_t)__popc(peers & ltm);
             __syncwarp();
-            if (valid && r == 0) wc[d] = (uint16_t)(before + __popc(pm[j]));
+            if (valid && r == 0) wc[d] = (uint16_t)(before + __popc(peers));
             __syncwarp();
             rd[j] = ((before + r) << 8) | d;
         }
@@ -389,10 +381,11 @@ struct Sorter {
         csync();
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) {
-            if (wbase + j * 32 + lane < m) {
+            const int idx = wbase + j * 32 + lane;
+            if (idx < m) {
                 const uint32_t pos = (uint32_t)wc[rd[j] & 0xFFu] + (rd[j] >> 8);
-                kd[pos] = k[j];
-                if (KV) vd[pos] = v[j];
+                kd[pos] = ks[idx];
+                if (KV) vd[pos] = vs[idx];
             }
         }
         csync();
@@ -589,13 +582,72 @@ struct Sorter {
         return reuse_sid >= 0;
     }
 
+    // ---- K5 radix exchange: split [b, e) on composite bit `bit` (0 = most significant) ---------------
+    // Every element shares the prefix (pk, pv) above `bit`; the threshold prefix|bit sends elements
+    // with a 0 bit left.  Returns true iff the reusable descriptor was consumed.
+    __device__ static bool radix_split(const Params &P, int64_t b, int64_t e, bool srcB, int bit, uint64_t pk,
+                                       uint32_t pv, int depth, int reuse_sid) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x;
+        const int64_t m = e - b;
+        if (m <= 0) return false;
+        if (bit >= NBITS || m == 1) {  // every bit decided: the elements are identical
+            finish_constant(P, b, e, srcB);
+            return false;
+        }
+        if (m <= P.base_size) {
+            Bnd nb{};
+            return spawn(P, b, e, srcB, nb, 1, depth, false, reuse_sid);  // leaf
+        }
+        uint64_t tk = pk;
+        uint32_t tv = pv;
+        if (bit < KBITS)
+            tk |= (uint64_t)((U)1 << (KBITS - 1 - bit));
+        else
+            tv |= 1u << (31 - (bit - KBITS));
+        const uint32_t ntiles = (uint32_t)((e - 1) / TILE - b / TILE + 1);
+        if (tid == 0) {
+            const uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
+            sh.new_sid = sid;
+            if (sid >= P.seg_cap) {
+                fail(P, -6);
+            } else {
+                Seg *s = &P.segs[sid];
+                s->begin = b;
+                s->end = e;
+                s->pivot = (uint64_t)O::from((U)tk);  // raw bits: tiles compare raw keys
+                s->pivot_v = tv;
+                s->lb = pk;
+                s->lb_v = pv;
+                s->ntiles = ntiles;
+                s->info = (srcB ? I_SRC_B : 0) | I_RADIX;
+                s->rbit = (unsigned)bit;
+                s->budget = 0;
+                s->depth = depth;
+                s->cnt_left = 0;
+                s->cnt_right = 0;
+                s->cnt_eq = 0;
+                s->tiles_done = 0;
+                __threadfence();
+                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)((ntiles + CHUNK - 1) / CHUNK));
+            }
+        }
+        csync();
+        if (sh.new_sid < P.seg_cap) push_tasks(P, T_PART, sh.new_sid, (ntiles + CHUNK - 1) / CHUNK);
+        csync();
+        if (depth > sh.s_max_depth && tid == 0) sh.s_max_depth = depth;
+        return reuse_sid >= 0;
+    }
+
     // ---- K1 + segment creation ------------------------------------------------------------
     // Creates the child segment [b, e) whose data lives in buffer srcB.  Small children are
     // finished right here (K7); big ones get a sampled pivot and their tiles are pushed.
     // Returns true iff the reusable descriptor `reuse_sid` was consumed.
-    __device__ static bool spawn(const Params &P, int64_t b, int64_t e, bool srcB,
-                                 bool has_lb, uint64_t lb, uint32_t lbv, int budget, int depth, bool perturb,
-                                 int reuse_sid, int rbyte) {
+    __device__ static bool spawn(const Params &P, int64_t b, int64_t e, bool srcB, const Bnd &bd, int budget,
+                                 int depth, bool perturb, int reuse_sid) {
+        const bool has_lb = bd.has_lb;
+        const uint64_t lb = bd.lb;
+        const uint32_t lbv = bd.lbv;
         Shared &sh = g_sh;
         const int tid = threadIdx.x;
         const int64_t m = e - b;
@@ -635,14 +687,25 @@ struct Sorter {
             csync();
             return false;
         }
-        // K5: the bad-partition budget is spent (driver.py:209-213): split the segment on its next
-        // radix digit instead of partitioning it again.  If the histogram pool is exhausted the
-        // segment keeps quicksorting with perturbed samples.
-        if (budget <= 0 && rbyte < NBYTES) {
+        // K5: the bad-partition budget is spent (driver.py:209-213, heapsort in the reference): the
+        // segment leaves quicksort for radix exchange, i.e. it is split on its most significant
+        // undecided bit by the same partition kernel; the work is bounded by the key width.
+        if (budget <= 0) {
             if (tid == 0) sh.s_fallback++;
-            const int r = radix_start(P, b, e, srcB, rbyte, depth, reuse_sid);
-            if (r >= 0) return r > 0;
-            perturb = true;
+            int bit = 0;
+            uint64_t pk = 0;
+            uint32_t pv = 0;
+            if (bd.has_lb && bd.has_ub) {  // lb <= e < ub: the common prefix of lb and ub is fixed
+                if (bd.lb != bd.ub) {
+                    bit = clz_u((U)(bd.lb ^ bd.ub));
+                    pk = bit ? (bd.lb & ~((uint64_t)(~(U)0) >> bit)) : 0;
+                } else {
+                    bit = KBITS + (KV ? (bd.lbv != bd.ubv ? __clz(bd.lbv ^ bd.ubv) : 32) : 0);
+                    pk = bd.lb;
+                    pv = (KV && bit > KBITS) ? (bit - KBITS >= 32 ? bd.lbv : (bd.lbv & ~(0xFFFFFFFFu >> (bit - KBITS)))) : 0u;
+                }
+            }
+            return radix_split(P, b, e, srcB, bit, pk, pv, depth, reuse_sid);
         }
         // K1: stratified samples (64, or SAMPLES for segments of 2^20+ keys); perturbed strata
         // after a bad partition.  The median of the sorted sample is the pivot.
@@ -713,10 +776,12 @@ struct Sorter {
                 s->lb_v = lbv;
                 s->ntiles = ntiles;
                 s->info = (srcB ? I_SRC_B : 0) | (left ? I_LEFT : 0) | (has_lb ? I_HAS_LB : 0) |
+                          (bd.has_ub ? I_HAS_UB : 0) |
                           (perturb ? I_PERTURB : 0) | (dup_heavy ? I_COUNT_EQ : 0);
                 s->budget = budget > 0 ? budget : 0;
                 s->depth = depth;
-                s->rbyte = (unsigned)rbyte;
+                s->ub = bd.ub;
+                s->ub_v = bd.ubv;
                 s->cnt_left = 0;
                 s->cnt_right = 0;
                 s->cnt_eq = 0;
@@ -748,6 +813,21 @@ struct Sorter {
         const int64_t b = sg.begin, e = sg.end, m = e - b, L = sh.fL;
         const bool srcB = sg.info & I_SRC_B, dstB = !srcB;
         const uint64_t piv_ord = (uint64_t)O::to((U)sg.pivot);
+        if (sg.info & I_RADIX) {
+            // K5 radix exchange: both sides continue on the next bit
+            if (tid == 0) sh.s_part_right++;
+            const int bit = (int)sg.rbit;
+            bool used = radix_split(P, b, b + L, dstB, bit + 1, sg.lb, sg.lb_v, sg.depth + 1, (int)sid);
+            radix_split(P, b + L, e, dstB, bit + 1, piv_ord, sg.pivot_v, sg.depth + 1, used ? -1 : (int)sid);
+            return;
+        }
+        Bnd parent{};
+        parent.has_lb = sg.info & I_HAS_LB;
+        parent.lb = sg.lb;
+        parent.lbv = sg.lb_v;
+        parent.has_ub = sg.info & I_HAS_UB;
+        parent.ub = sg.ub;
+        parent.ubv = sg.ub_v;
         if (!(sg.info & I_LEFT)) {
             if (tid == 0) sh.s_part_right++;
             if (sh.fE == m) {
@@ -763,10 +843,15 @@ struct Sorter {
             if (tid == 0 && bad) sh.s_bad++;
             const int nb = sg.budget - (bad ? 1 : 0);
             const bool perturb = bad && P.use_break;
-            bool used = spawn(P, b, b + L, dstB, sg.info & I_HAS_LB, sg.lb, sg.lb_v, nb, sg.depth + 1,
-                              perturb, (int)sid, (int)sg.rbyte);
-            spawn(P, b + L, e, dstB, true, piv_ord, sg.pivot_v, nb, sg.depth + 1, perturb,
-                  used ? -1 : (int)sid, (int)sg.rbyte);
+            Bnd lbd = parent, rbd = parent;  // left: [lb, pivot), right: [pivot, ub)
+            lbd.has_ub = true;
+            lbd.ub = piv_ord;
+            lbd.ubv = sg.pivot_v;
+            rbd.has_lb = true;
+            rbd.lb = piv_ord;
+            rbd.lbv = sg.pivot_v;
+            bool used = spawn(P, b, b + L, dstB, lbd, nb, sg.depth + 1, perturb, (int)sid);
+            spawn(P, b + L, e, dstB, rbd, nb, sg.depth + 1, perturb, used ? -1 : (int)sid);
         } else {
             if (tid == 0) sh.s_part_left++;
             bool used = false;
@@ -777,159 +862,14 @@ struct Sorter {
             } else {
                 used = fill_final(P, b, b + L, piv_ord, sg.pivot_v, (int)sid);
             }
-            spawn(P, b + L, e, dstB, true, piv_ord, sg.pivot_v, sg.budget, sg.depth + 1, false,
-                  used ? -1 : (int)sid, (int)sg.rbyte);
+            Bnd rbd = parent;  // (pivot, ub): the pivot is a valid lower bound
+            rbd.has_lb = true;
+            rbd.lb = piv_ord;
+            rbd.lbv = sg.pivot_v;
+            spawn(P, b + L, e, dstB, rbd, sg.budget, sg.depth + 1, false, used ? -1 : (int)sid);
         }
     }
 
-    // ---- K5: MSD radix split (the fallback) -----------------------------------------------------------
-    // Phase 1 (T_RHIST tiles): 256-bin histogram of digit `rbyte`.  Phase 2 (T_RSCAT tiles): every
-    // tile reserves its per-bucket runs with one atomic per non-empty bucket and scatters into the
-    // other buffer.  Buckets then resume quicksort with a fresh budget and the next digit, so a
-    // sustained adversary costs at most one split per digit along any path.
-    // Returns 1 if `reuse_sid` was consumed, 0 if not, -1 if no histogram slot was free.
-    __device__ static int radix_start(const Params &P, int64_t b, int64_t e, bool srcB, int rbyte, int depth,
-                                      int reuse_sid) {
-        Shared &sh = g_sh;
-        const int tid = threadIdx.x;
-        if (tid == 0) sh.new_sid = atomicAdd(&P.st->hpool_alloc, 1u);
-        csync();
-        const uint32_t hs = sh.new_sid;
-        csync();
-        if (hs >= P.hpool_cap) return -1;
-        uint32_t *h = P.hpool + (size_t)hs * HSLOT;
-        for (int i = tid; i < HSLOT; i += THREADS) h[i] = 0u;
-        __threadfence();
-        csync();
-        const uint32_t ntiles = (uint32_t)((e - 1) / TILE - b / TILE + 1);
-        const uint32_t nchunks = (ntiles + CHUNK - 1) / CHUNK;
-        if (tid == 0) {
-            const uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
-            sh.new_sid = sid;
-            if (sid >= P.seg_cap) {
-                fail(P, -6);
-            } else {
-                Seg *s = &P.segs[sid];
-                s->begin = b;
-                s->end = e;
-                s->info = I_RADIX | (srcB ? I_SRC_B : 0u);
-                s->rbyte = (unsigned)rbyte;
-                s->hidx = hs;
-                s->ntiles = ntiles;
-                s->depth = depth;
-                s->budget = 0;
-                s->tiles_done = 0;
-                __threadfence();
-                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)nchunks);
-            }
-        }
-        csync();
-        if (sh.new_sid < P.seg_cap) push_tasks(P, T_RHIST, sh.new_sid, nchunks);
-        csync();
-        return reuse_sid >= 0 ? 1 : 0;
-    }
-
-    __device__ static void rhist_tile(const Params &P, uint32_t tile, unsigned &ci) {
-        Shared &sh = g_sh;
-        const int tid = threadIdx.x;
-        const Seg &sg = sh.seg;
-        const int64_t tbase = (sg.begin / TILE + tile) * (int64_t)TILE;
-        const int lo_i = (int)((sg.begin > tbase ? sg.begin : tbase) - tbase);
-        const int hi_i = (int)((sg.end < tbase + TILE ? sg.end : tbase + TILE) - tbase);
-        const int st = (int)(ci % NST);
-        mbar_wait(&sh.bar[st], (ci / NST) & 1u);
-        ++ci;
-        uint32_t *hist = reinterpret_cast<uint32_t *>(B::kc());
-        csync();  // the previous tile may still be reading kc
-        hist[tid] = 0u;
-        csync();
-        const U *sk = B::stage(st);
-        const uint32_t *sv = KV ? B::vstage(st) : nullptr;
-        const int rb = (int)sg.rbyte;
-        for (int i = lo_i + tid; i < hi_i; i += THREADS) atomicAdd(&hist[rdigit(sk[i], KV ? sv[i] : 0u, rb)], 1u);
-        csync();  // stage consumed
-        if (tid == 0) {
-            sh.ci = ci;
-            pump_loads(P);
-            sh.s_tiles++;
-            sh.s_bytes += (unsigned long long)ELEM_BYTES * (hi_i - lo_i);
-        }
-        const uint32_t c = hist[tid];
-        if (c) atomicAdd(&P.hpool[(size_t)sg.hidx * HSLOT + 256 + tid], c);
-    }
-
-    __device__ static void rscat_tile(const Params &P, uint32_t tile, unsigned &ci) {
-        Shared &sh = g_sh;
-        const int tid = threadIdx.x;
-        const Seg &sg = sh.seg;
-        const int64_t tbase = (sg.begin / TILE + tile) * (int64_t)TILE;
-        const int lo_i = (int)((sg.begin > tbase ? sg.begin : tbase) - tbase);
-        const int hi_i = (int)((sg.end < tbase + TILE ? sg.end : tbase + TILE) - tbase);
-        const bool srcB = sg.info & I_SRC_B;
-        U *dst = (U *)(srcB ? P.a_keys : P.b_keys);
-        uint32_t *dstv = srcB ? P.a_vals : P.b_vals;
-        const int st = (int)(ci % NST);
-        mbar_wait(&sh.bar[st], (ci / NST) & 1u);
-        ++ci;
-        uint32_t *hist = reinterpret_cast<uint32_t *>(B::kc());
-        csync();  // the previous tile may still be reading kc
-        hist[tid] = 0u;
-        csync();
-        const U *sk = B::stage(st);
-        const uint32_t *sv = KV ? B::vstage(st) : nullptr;
-        const int rb = (int)sg.rbyte;
-        U k[ITEMS];
-        uint32_t v[ITEMS], pk[ITEMS];
-#pragma unroll
-        for (int r = 0; r < ITEMS; ++r) {
-            const int i = r * THREADS + tid;
-            const bool valid = i >= lo_i && i < hi_i;
-            k[r] = sk[i];
-            v[r] = KV ? sv[i] : 0u;
-            const uint32_t d = rdigit(k[r], v[r], rb);
-            pk[r] = valid ? (d | atomicAdd(&hist[d], 1u) << 8) : 0xFFFFFFFFu;  // rank within the tile
-        }
-        csync();  // stage consumed, tile histogram complete
-        if (tid == 0) {
-            sh.ci = ci;
-            pump_loads(P);
-            sh.s_tiles++;
-            sh.s_bytes += 2ull * ELEM_BYTES * (hi_i - lo_i);
-        }
-        const uint32_t c = hist[tid];
-        const uint32_t base = c ? atomicAdd(&P.hpool[(size_t)sg.hidx * HSLOT + tid], c) : 0u;
-        csync();
-        hist[tid] = base;
-        csync();
-#pragma unroll
-        for (int r = 0; r < ITEMS; ++r) {
-            if (pk[r] != 0xFFFFFFFFu) {
-                const int64_t pos = sg.begin + hist[pk[r] & 255u] + (pk[r] >> 8);
-                dst[pos] = k[r];
-                if (KV) dstv[pos] = v[r];
-            }
-        }
-        csync();
-    }
-
-    // block-wide exclusive scan of one u32 per thread (THREADS == 256 == radix bins)
-    __device__ static uint32_t block_excl_scan(uint32_t x) {
-        Shared &sh = g_sh;
-        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-        uint32_t inc = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        csync();
-        if (lane == 31) sh.scan[warp] = inc;
-        csync();
-        uint32_t pre = inc - x;
-#pragma unroll
-        for (int q = 0; q < WARPS; ++q) pre += (q < warp) ? sh.scan[q] : 0u;
-        return pre;
-    }
 
     // Every key of [b, e) (in buffer srcB) is bitwise identical: make A hold it.
     __device__ static void finish_constant(const Params &P, int64_t b, int64_t e, bool srcB) {
@@ -940,72 +880,6 @@ struct Sorter {
         } else {
             if (threadIdx.x == 0) finish_keys(P, (unsigned long long)(e - b));
             csync();
-        }
-    }
-
-    __device__ __noinline__ static void finalize_rhist(const Params &P, const Seg &sg, uint32_t sid) {
-        Shared &sh = g_sh;
-        const int tid = threadIdx.x;
-        const int64_t b = sg.begin, e = sg.end, m = e - b;
-        uint32_t *h = P.hpool + (size_t)sg.hidx * HSLOT;
-        const uint32_t c = __ldcg(&h[256 + tid]);
-        const uint32_t nchunks = (sg.ntiles + CHUNK - 1) / CHUNK;
-        if (csync_or((int64_t)c == m)) {
-            // one bucket holds everything: this digit carries no information
-            if ((int)sg.rbyte + 1 >= NBYTES) {
-                finish_constant(P, b, e, sg.info & I_SRC_B);
-                return;
-            }
-            h[256 + tid] = 0u;
-            __threadfence();
-            csync();
-            if (tid == 0) {
-                Seg *s = &P.segs[sid];
-                s->rbyte = sg.rbyte + 1;
-                s->tiles_done = 0;
-                __threadfence();
-                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)nchunks);
-            }
-            csync();
-            push_tasks(P, T_RHIST, sid, nchunks);
-            csync();
-            return;
-        }
-        h[tid] = block_excl_scan(c);  // bucket cursors (relative to begin)
-        __threadfence();
-        csync();
-        if (tid == 0) {
-            Seg *s = &P.segs[sid];
-            s->tiles_done = 0;
-            __threadfence();
-            sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)nchunks);
-        }
-        csync();
-        push_tasks(P, T_RSCAT, sid, nchunks);
-        csync();
-    }
-
-    __device__ __noinline__ static void finalize_rscat(const Params &P, const Seg &sg, uint32_t sid) {
-        const int tid = threadIdx.x;
-        const int64_t b = sg.begin;
-        const bool dstB = !(sg.info & I_SRC_B);
-        // bucket counts and start offsets stay in the parent's histogram slot (children take new
-        // slots); shared memory cannot hold them because spawned children sample into kc
-        const uint32_t *h = P.hpool + (size_t)sg.hidx * HSLOT;
-        if (tid == 0) g_sh.s_part_right++;
-        const int nrb = (int)sg.rbyte + 1;
-        bool reused = false;
-        for (int d = 0; d < 256; ++d) {
-            const uint32_t cd = __ldcg(&h[256 + d]);
-            if (!cd) continue;
-            const int64_t cb = b + (__ldcg(&h[d]) - cd);  // the cursor advanced by exactly the count
-            if (nrb >= NBYTES) {
-                finish_constant(P, cb, cb + cd, dstB);  // every digit matched: identical elements
-            } else {
-                const int budget = 63 - __clzll((long long)cd);  // a fresh budget for the bucket
-                reused |= spawn(P, cb, cb + cd, dstB, false, 0, 0, budget, sg.depth + 1, false,
-                                reused ? -1 : (int)sid, nrb);
-            }
         }
     }
 
@@ -1235,7 +1109,7 @@ struct Sorter {
 
     // thread 0: keep NST tile loads in flight ahead of the compute side, walking the current task's
     // chunk and then, once it is published, the next task's chunk.
-    __device__ static void pump_loads(const Params &P) {
+    __device__ __forceinline__ static void pump_loads(const Params &P) {
         Shared &sh = g_sh;
         while (sh.li < sh.ci + NST) {
             if (sh.lslot == 0) {
@@ -1425,7 +1299,8 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
     if (s_action == 0) {
         int budget = P.budget0;
         if (budget < 0) budget = 63 - __clzll((long long)P.n);  // driver.py:263: n.bit_length() - 1
-        S::spawn(P, 0, P.n, false, false, 0, 0, budget, 0, false, -1, 0);
+        typename S::Bnd none{};
+        S::spawn(P, 0, P.n, false, none, budget, 0, false, -1);
     }
     __syncthreads();
     if (tid == 0) S::flush_counters(P);
@@ -1509,17 +1384,10 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
         if (!w) break;
         const uint32_t type = (uint32_t)(w >> 45) & 7u;
         const uint32_t sid = (uint32_t)(w >> 23) & 0x3FFFFF;
-        if (S::tile_task(type)) {
+        if (type == T_PART) {
             const uint32_t t0 = ((uint32_t)w & 0x7FFFFF) * CHUNK;
             const uint32_t t1 = min(t0 + CHUNK, sh.seg.ntiles);
-            for (uint32_t t = t0; t < t1; ++t) {
-                if (type == T_PART)
-                    S::part_tile(P, sid, t, ci);
-                else if (type == T_RHIST)
-                    S::rhist_tile(P, t, ci);
-                else
-                    S::rscat_tile(P, t, ci);
-            }
+            for (uint32_t t = t0; t < t1; ++t) S::part_tile(P, sid, t, ci);
             // retire the chunk: one gpu-scope fence per thread, one counter update per CTA
             __threadfence();
             csync();
@@ -1532,12 +1400,7 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
             csync();
             if (sh.last) {
                 __threadfence();
-                if (type == T_PART)
-                    S::finalize_part(P, sh.seg, sid);
-                else if (type == T_RHIST)
-                    S::finalize_rhist(P, sh.seg, sid);
-                else
-                    S::finalize_rscat(P, sh.seg, sid);
+                S::finalize_part(P, sh.seg, sid);
             }
         } else {  // T_FILL
             S::fill_tile(P, sh.seg, (uint32_t)w & 0x7FFFFF);
