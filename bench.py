@@ -46,6 +46,21 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
+    (profiles/*_ncu_kernels.json, written from the same bench command), or None."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_kernels.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        d = json.load(f).get(kernel)
+    if not d:
+        return None, None
+    return (d["dram_read_GB"] + d["dram_write_GB"]) * 1e9, os.path.relpath(files[-1], ROOT)
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -72,7 +87,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -81,7 +96,12 @@ class Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def wait_first(self, timeout=10.0):
+        t0 = time.perf_counter()
+        while self.proc and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
 
     def __exit__(self, *a):
         if self.proc:
@@ -91,10 +111,19 @@ class Clocks:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
+        """Median SM clock and active throttle reasons over samples taken in [t0, t1]
+        (widened to the nearest samples on either side if the window is shorter than
+        the sampling period)."""
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        sel = self.lines
+        if t0 is not None and self.lines:
+            before = [x for x in self.lines if x[0] < t0]
+            inside = [x for x in self.lines if t0 <= x[0] <= t1]
+            after = [x for x in self.lines if x[0] > t1]
+            sel = before[-1:] + inside + after[:1]
+        for _, ln in sel:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -132,6 +161,22 @@ def cpu_reference_sample(n_sample: int, min_seconds: float, seed_offset: int = 6
         total_keys += n_sample
         sorts += 1
     return total_keys / total_t, total_t, sorts
+
+
+def reduce_max_ms(ms: float, dist, device) -> float:
+    """Max over ranks of a per-rank device time (the contract's multi-GPU clock)."""
+    if dist is None:
+        return float(ms)
+    import torch
+
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def weak_scaling_value(n_per_rank: int, steps: int, world: int, max_ms: float) -> float:
+    """Whole-job keys/s: every rank sorts its own replica of n keys per step."""
+    return n_per_rank * steps * world / (max_ms / 1e3)
 
 
 def run_reference(args, rank, world):
@@ -209,6 +254,9 @@ def run_ours(args, rank, world, local_rank):
         if pristine is not None:
             inputs[i % n_inputs].copy_(pristine[i % n_inputs])
 
+    clocks = Clocks(local_rank)
+    clocks.__enter__()
+    clocks.wait_first()
     # warmup (untimed)
     for i in range(W):
         restore(i)
@@ -224,9 +272,8 @@ def run_ours(args, rank, world, local_rank):
         pair[1].record(stream)
     torch.cuda.synchronize()
     step_stats = []
-    clocks = Clocks(local_rank)
     t_wall0 = time.perf_counter()
-    with clocks:
+    try:
         start_all = torch.cuda.Event(enable_timing=True)
         end_all = torch.cuda.Event(enable_timing=True)
         start_all.record(stream)
@@ -239,7 +286,11 @@ def run_ours(args, rank, world, local_rank):
                 restore(W + s + 1)
         end_all.record(stream)
         torch.cuda.synchronize()
-    t_wall = time.perf_counter() - t_wall0
+        t_wall1 = time.perf_counter()
+        time.sleep(0.12)  # let the sampler report the tail of the timed region
+    finally:
+        clocks.__exit__(None, None, None)
+    t_wall = t_wall1 - t_wall0
     if pristine is None:
         stats = ds.finish()
     else:
@@ -247,11 +298,7 @@ def run_ours(args, rank, world, local_rank):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ksort_ms = [a.elapsed_time(b) for a, b in kev]
     total_ms = sum(step_ms) if pristine is not None else start_all.elapsed_time(end_all)
-    # max over ranks (device time)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = reduce_max_ms(total_ms, dist, dev)
     barrier()
 
     # verify the last timed output (cheap device check)
@@ -272,10 +319,11 @@ def run_ours(args, rank, world, local_rank):
 
     if rank == 0:
         peak, peak_src = peaks()
-        value = n * K * world / (total_ms / 1e3)
+        value = weak_scaling_value(n, K, world, total_ms)
         # roofline of the dominant kernel (the persistent sorter k_sort): algorithmic bytes per launch
         # (device counter, SURVEY.md §8(d) byte model over the segments it processed) / its event time
         bytes_launch = stats["bytes_algorithmic"]
+        traffic, traffic_src = ncu_traffic("k_sort")
         ks_ms = statistics.mean(ksort_ms)
         achieved = bytes_launch / (ks_ms / 1e3) / 1e9
         line = {
@@ -301,14 +349,15 @@ def run_ours(args, rank, world, local_rank):
             },
             "roofline": {
                 "bound": "hbm",
-                "kernel": "k_sort (persistent partition/base-case sorter)",
+                "kernel": "k_sort (persistent segment-queue partition kernel: K1-K6)",
                 "achieved": achieved,
                 "peak": peak,
                 "peak_source": peak_src,
                 "unit": "GB/s",
                 "frac": achieved / peak,
                 "frac_vs_8tbs": achieved / 8000.0,
-                "traffic": None,
+                "traffic": traffic,
+                "traffic_source": traffic_src,
                 "bytes_algorithmic_per_launch": bytes_launch,
                 "bytes_per_key": bytes_launch / n,
                 "kernel_ms": ks_ms,
@@ -318,7 +367,7 @@ def run_ours(args, rank, world, local_rank):
             },
             "gpu_launches": 4 * K,
             "device_counters": stats,
-            "clocks": clocks.summary(),
+            "clocks": clocks.summary(t_wall0, t_wall1),
             "wall_s_timed_region": t_wall,
         }
         if e2e is not None:
