@@ -1,22 +1,23 @@
 // pdq_kernels.cuh — the seven kernels of the B200 pdqsort path.
 //
-//   K1 sample pivot          spawn(): SAMPLES stratified keys, CTA bitonic, median
-//                            (generalises choose_pivot, driver.py:81-113)
-//   K2 partition_right       part_tile(): TMA bulk tile -> classify -> ballot/popc ranks ->
-//                            block scan -> one atomic per CTA for both sides -> shared-memory
-//                            compaction -> 16 B stores (block_partition_right, partition.py:184-301)
+//   K1 sample pivot          spawn(): 64 (256 for >= 2^20 keys) stratified samples, warp/CTA
+//                            bitonic, median (generalises choose_pivot, driver.py:81-113)
+//   K2 partition_right       part_tile(): TMA bulk tile -> classify -> block scan -> one packed
+//                            atomic per tile for both sides -> shared-memory compaction -> 16 B
+//                            stores (block_partition_right, partition.py:184-301)
 //   K3 partition_left        part_tile() in I_LEFT mode (partition.py:128-181, driver.py:222-225)
 //   K4 sortedness check      k_check(): adjacent-compare reduction; k_sort prologue reverses
 //                            non-increasing input (partial_insertion_sort path, driver.py:244-250)
 //   K5 bad-partition budget  finalize_part(): is_bad_partition (driver.py:116-124), budget,
-//                            sample perturbation (break_patterns, driver.py:127-156)
-//   K6 segment queue         k_sort(): persistent, warp-specialised CTAs.  A scheduler warp claims
-//                            tasks from the device ring, issues the TMA bulk loads into a 2-stage
-//                            mbarrier pipeline and retires finished tiles (fence + counter); eight
-//                            compute warps partition tiles and run finalizations (driver.py:198-260)
-//   K7 base case             base_case(): segment <= base_case_size sorted in shared memory by a
-//                            range-reduced LSD radix sort (insertion_sort / unguarded_insertion_sort,
-//                            small_sorts.py:16-73)
+//                            sample perturbation (break_patterns, driver.py:127-156); an exhausted
+//                            budget switches the segment to radix exchange (heapsort's role)
+//   K6 segment queue         k_sort(): persistent CTAs claim chunks of 8 tiles from a device ring of
+//                            64-bit task words, prefetch the next tile by TMA while storing the
+//                            current one, retire chunks with one fence + counter; the last chunk's
+//                            CTA finalizes the segment and spawns its children (driver.py:198-260)
+//   K7 base case             k_base() / leaf_loop(): leaves <= base_case_size sorted by a one-pass
+//                            bucket sort + per-thread insertion runs, radix passes for clustered
+//                            leaves (insertion_sort / unguarded_insertion_sort, small_sorts.py:16-73)
 #pragma once
 
 #include "pdq_device.cuh"
@@ -31,8 +32,16 @@ constexpr int NST = PDQ_NST;            // TMA stages: tile loads run up to NST 
 constexpr int RADIX_BITS = 8;
 constexpr int RADIX_DIGITS = 1 << RADIX_BITS;
 constexpr int CNT_BYTES = RADIX_DIGITS * WARPS * 2;  // per-warp u16 digit counters
+#ifndef PDQ_BUCKET_BITS
+#define PDQ_BUCKET_BITS 11
+#endif
+#ifndef PDQ_KB_SKIP
+#define PDQ_KB_SKIP 0
+#endif
+constexpr int BUCKET_MAX = 24;  // larger buckets (clustered / repeated keys): radix passes instead
+constexpr int RUN_MAX = 64;     // longest per-thread insertion run (8 buckets) accepted
 
-// compute-warp barrier (named barrier 1): the scheduler warp never joins it
+// CTA barrier (named barrier 1, all THREADS threads)
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(THREADS) : "memory"); }
 __device__ __forceinline__ int csync_or(int p) {
     int r;
@@ -63,6 +72,7 @@ struct Shared {
     uint64_t ntask;          // prefetched next task (0 = none / not yet published)
     Seg nseg;
     unsigned long long npos; // ring position claimed for the next task
+    uint64_t lf[2];          // K7: descriptors of the current and the next leaf
     int nstate;              // 0 none, 1 claimed (unpublished), 2 ready, 3 exit
     // load cursor (thread 0): tiles issued so far, and which task/tile is the next to load
     unsigned li;             // loads issued (stage li % NST)
@@ -131,7 +141,11 @@ struct BaseBufs {
         return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES) + MAX_BASE;
     }
     __device__ __forceinline__ static uint16_t *cnt() { return reinterpret_cast<uint16_t *>(g_dsm + KEY_BYTES + VAL_BYTES); }
-    __host__ __device__ static constexpr int bytes() { return KEY_BYTES + VAL_BYTES + CNT_BYTES; }
+    __device__ __forceinline__ static uint32_t *bkt() { return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES + VAL_BYTES); }
+    // K7 bucket count: 4096 for 4-byte keys, 2048 for wider elements (keeps 2 CTAs/SM there)
+    static constexpr int BK = 1 << ((sizeof(U) == 4 && !KV) ? PDQ_BUCKET_BITS : 11);
+    static constexpr int CNT_AREA = CNT_BYTES > BK * 4 ? CNT_BYTES : BK * 4;
+    __host__ __device__ static constexpr int bytes() { return KEY_BYTES + VAL_BYTES + CNT_AREA; }
 };
 
 template <class U, bool FLOAT, bool KV>
@@ -400,29 +414,107 @@ struct Sorter {
         return __clzll((long long)x);
     }
 
-    __device__ __noinline__ static void base_case(const Params &P, bool srcB, int64_t b,
-                                                  int m) {
+    __device__ __forceinline__ static U *kbuf(int c) { return c ? BB::kc() : BB::kx(); }
+    __device__ __forceinline__ static uint32_t *vbuf(int c) { return KV ? (c ? BB::vc() : BB::vx()) : nullptr; }
+
+    // Radix path of the leaf sort (kx/vx hold the leaf): stable 8-bit LSD passes over (key - mn); a KV
+    // leaf with repeated keys first orders by payload.  Returns the buffer index holding the result.
+    __device__ __noinline__ static int radix_leaf(int m, U mn, U range, uint32_t vmn, uint32_t vmx) {
+        const int tid = threadIdx.x;
+        const int kbits = range ? (int)(sizeof(U) * 8) - clz_u(range) : 0;
+        int c = 0;
+        for (int s = 0; s < kbits; s += RADIX_BITS, c ^= 1)
+            radix_pass(kbuf(c), vbuf(c), kbuf(c ^ 1), vbuf(c ^ 1), m, mn, s, false, 0);
+        if (KV && vmx != vmn) {
+            // keys repeat? then order equal keys by payload: payload passes, then key passes again
+            int dup = 0;
+            const U *ck = kbuf(c);
+            for (int i = tid; i + 1 < m; i += THREADS) dup |= (ck[i] == ck[i + 1]);
+            if (csync_or(dup)) {
+                const int vbits = 32 - __clz(vmx - vmn);
+                for (int s = 0; s < vbits; s += RADIX_BITS, c ^= 1)
+                    radix_pass(kbuf(c), vbuf(c), kbuf(c ^ 1), vbuf(c ^ 1), m, mn, s, true, vmn);
+                for (int s = 0; s < kbits; s += RADIX_BITS, c ^= 1)
+                    radix_pass(kbuf(c), vbuf(c), kbuf(c ^ 1), vbuf(c ^ 1), m, mn, s, false, 0);
+            }
+        }
+        return c;
+    }
+
+    // Issue the register loads of one leaf (descriptor lf; ~0 = none): thread t gets elements t + 256 j.
+    __device__ __forceinline__ static void load_leaf(const Params &P, uint64_t lf, U (&xs)[ITEMS],
+                                                     uint32_t (&vs)[KV ? ITEMS : 1]) {
+        const int tid = threadIdx.x;
+        const int m = lf == ~0ull ? 0 : (int)((lf >> 1) & 0x1FFF) + 1;
+        const int64_t b = (int64_t)(lf >> 14);
+        const U *src = (const U *)((lf & 1u) ? P.b_keys : P.a_keys);
+        const uint32_t *srcv = (lf & 1u) ? P.b_vals : P.a_vals;
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            const int i = j * THREADS + tid;
+            xs[j] = i < m ? ldcg(src + b + i) : (U)0;
+            if constexpr (KV) vs[j] = i < m ? ldcg(srcv + b + i) : 0u;
+        }
+    }
+
+    // K7 leaf sort (segment of m <= 4096 keys).  The leaf is loaded into registers (16 keys per thread,
+    // all loads in flight at once) and range-reduced to [mn, mn + range].  Fast path, a one-pass bucket
+    // sort: a monotone scaling of (key - mn) picks one of 2048 buckets, a shared-memory atomic gives
+    // every key its slot in its bucket, one scan turns counts into bucket offsets and the keys go
+    // straight from registers to their bucket in kc.  Thread t's buckets [8t, 8t + 8) form one
+    // contiguous run of kc that is already ordered between buckets, so one insertion sort of the run
+    // (ordering (key, payload) pairs) finishes the leaf.  A 2.8K-key leaf of a uniform sort has ~1.4
+    // keys per bucket: about one warp instruction per key, instead of one radix pass per 8 key bits.
+    // When a bucket holds more than BUCKET_MAX keys or a run exceeds RUN_MAX (clustered or repeated
+    // keys), the leaf goes through the stable 8-bit radix passes instead.
+    // The leaf loop is software-pipelined: a leaf's keys are loaded into registers while the previous
+    // leaf is insertion-sorted and stored, and thread 0 claims the following leaf (one atomic on the leaf
+    // queue + one descriptor load) while the current one is bucketed.
+    __device__ __noinline__ static void leaf_loop(const Params &P) {
         Shared &sh = g_sh;
         const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        uint32_t *cnt = BB::bkt();
+        unsigned long long count = *(volatile unsigned long long *)&P.st->leaf_count;
+        if (count > P.leaf_cap) count = P.leaf_cap;
+        constexpr uint64_t NONE = ~0ull;
+        auto claim = [&](int k) {
+            if (tid == 0) {
+                const unsigned long long idx = atomicAdd(&P.st->leaf_next, 1ull);
+                sh.lf[k] = idx < count ? ldcg(P.leaves + idx) : NONE;
+            }
+        };
+        U xs[ITEMS];
+        uint32_t vs[KV ? ITEMS : 1];
+        claim(0);
+        csync();
+        uint64_t cur = sh.lf[0];
+        int k = 0;
+        load_leaf(P, cur, xs, vs);
+        while (cur != NONE) {
         const long long c0 = clock64();
-        const U *src = (const U *)(srcB ? P.b_keys : P.a_keys);
-        const uint32_t *srcv = srcB ? P.b_vals : P.a_vals;
-        U *bufk[2] = {BB::kx(), BB::kc()};
-        uint32_t *bufv[2] = {KV ? BB::vx() : nullptr, KV ? BB::vc() : nullptr};
-        // coalesced load (ordered image), min/max of keys and payload
+        claim(k ^ 1);
+        const int m = (int)((cur >> 1) & 0x1FFF) + 1;
+        const int64_t b = (int64_t)(cur >> 14);
+        const int J = (m + THREADS - 1) / THREADS;
+        {  // zero the bucket counters while the loads are in flight
+            uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
+#pragma unroll
+            for (int q = 0; q < BB::BK / 4 / THREADS; ++q) c4[q * THREADS + tid] = make_uint4(0, 0, 0, 0);
+        }
+        // ordered image, min/max of keys and payload
         U mn = ~(U)0, mx = 0;
         uint32_t vmn = 0xFFFFFFFFu, vmx = 0;
-#pragma unroll 4
-        for (int i = tid; i < m; i += THREADS) {
-            const U x = O::to(ldcg(src + b + i));
-            bufk[0][i] = x;
-            mn = x < mn ? x : mn;
-            mx = x > mx ? x : mx;
-            if (KV) {
-                const uint32_t v = ldcg(srcv + b + i);
-                bufv[0][i] = v;
-                vmn = v < vmn ? v : vmn;
-                vmx = v > vmx ? v : vmx;
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            if (j < J && j * THREADS + tid < m) {
+                const U x = O::to(xs[j]);
+                xs[j] = x;
+                mn = x < mn ? x : mn;
+                mx = x > mx ? x : mx;
+                if constexpr (KV) {
+                    vmn = vs[j] < vmn ? vs[j] : vmn;
+                    vmx = vs[j] > vmx ? vs[j] : vmx;
+                }
             }
         }
 #pragma unroll
@@ -462,27 +554,135 @@ struct Sorter {
             }
         }
         const U range = mx - mn;
-        const int kbits = range ? (int)(sizeof(U) * 8) - clz_u(range) : 0;
-        int c = 0;  // index of the buffer holding the current order
-        for (int s = 0; s < kbits; s += RADIX_BITS, c ^= 1)
-            radix_pass(bufk[c], bufv[c], bufk[c ^ 1], bufv[c ^ 1], m, mn, s, false, 0);
-        if (KV && vmx != vmn) {
-            // keys repeat? then order equal keys by payload: payload passes, then key passes again
-            int dup = 0;
-            for (int i = tid; i + 1 < m; i += THREADS) dup |= (bufk[c][i] == bufk[c][i + 1]);
-            if (csync_or(dup)) {
-                const int vbits = 32 - __clz(vmx - vmn);
-                for (int s = 0; s < vbits; s += RADIX_BITS, c ^= 1)
-                    radix_pass(bufk[c], bufv[c], bufk[c ^ 1], bufv[c ^ 1], m, mn, s, true, vmn);
-                for (int s = 0; s < kbits; s += RADIX_BITS, c ^= 1)
-                    radix_pass(bufk[c], bufv[c], bufk[c ^ 1], bufv[c ^ 1], m, mn, s, false, 0);
+        bool ok = range != 0;  // uniform across the CTA
+#if PDQ_KB_SKIP == 2  // profiling build only: leaf copied unsorted (measures the load/store floor)
+        ok = false;
+#endif
+        // bucket(x) = floor(y * BUCKETS / (ry + 1)), y = (x - mn) >> s0 fitting 32 bits: monotone in x
+        const int s0 = (sizeof(U) == 8 && (uint64_t)range >> 32) ? 32 - __clz((uint32_t)((uint64_t)range >> 32)) : 0;
+        // (R from a float quotient, no division subroutine; rounding only shifts bucket edges, the clamp
+        // keeps the last bucket in range, and a constant factor keeps the map monotone)
+        const uint64_t R = (uint64_t)__fdividef((float)((uint64_t)BB::BK << 32), (float)(uint32_t)(range >> s0) + 1.0f);
+        auto bucket = [&](U x) -> uint32_t {
+            return min((uint32_t)(((uint64_t)(uint32_t)((x - mn) >> s0) * R) >> 32), (uint32_t)BB::BK - 1);
+        };
+        uint32_t slot[ITEMS / 2];  // two 16-bit bucket slots per register
+        int r0 = 0, r1 = 0;        // this thread's run [r0, r1) of kc
+        if (ok) {
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) {
+                uint32_t sl = 0;
+                if (j < J && j * THREADS + tid < m) sl = atomicAdd(&cnt[bucket(xs[j])], 1u);
+                if (j & 1) slot[j / 2] |= sl << 16;
+                else slot[j / 2] = sl;
             }
+            csync();
+            // exclusive scan of the bucket counts (thread t owns buckets [8t, 8t + 8)); largest bucket/run
+            constexpr int PER = BB::BK / THREADS;
+            uint32_t c[PER], tot = 0, big = 0;
+            const uint4 *c4 = reinterpret_cast<const uint4 *>(cnt + PER * tid);
+#pragma unroll
+            for (int q = 0; q < PER / 4; ++q) {
+                const uint4 y = c4[q];
+                c[4 * q] = y.x; c[4 * q + 1] = y.y; c[4 * q + 2] = y.z; c[4 * q + 3] = y.w;
+            }
+#pragma unroll
+            for (int q = 0; q < PER; ++q) { tot += c[q]; big = c[q] > big ? c[q] : big; }
+            uint32_t inc = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            big = __reduce_max_sync(0xffffffffu, big | (tot > (uint32_t)RUN_MAX ? 0x10000u : 0u));
+            if (lane == 31) { sh.scan[warp] = inc; sh.red_a[warp] = big; }
+            csync();
+            uint32_t run = inc - tot;
+            big = 0;
+#pragma unroll
+            for (int q = 0; q < WARPS; ++q) {
+                run += (q < warp) ? sh.scan[q] : 0u;
+                big = sh.red_a[q] > big ? sh.red_a[q] : big;
+            }
+            ok = big <= (uint32_t)BUCKET_MAX;
+            r0 = (int)run;
+            r1 = (int)(run + tot);
+            uint4 *w4 = reinterpret_cast<uint4 *>(cnt + PER * tid);
+#pragma unroll
+            for (int q = 0; q < PER / 4; ++q) {
+                uint4 y;
+                y.x = run; run += c[4 * q];
+                y.y = run; run += c[4 * q + 1];
+                y.z = run; run += c[4 * q + 2];
+                y.w = run; run += c[4 * q + 3];
+                w4[q] = y;
+            }
+            csync();
+        }
+        int c = 0;  // index of the buffer holding the current order (0: kx/vx, 1: kc/vc)
+        const uint64_t nxt = sh.lf[k ^ 1];  // written by thread 0 before the first barrier above
+        if (ok) {
+            U *kc = BB::kc();
+            uint32_t *vc = BB::vc();
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) {
+                if (j < J && j * THREADS + tid < m) {
+                    const uint32_t pos = cnt[bucket(xs[j])] + ((slot[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
+                    kc[pos] = xs[j];
+                    if constexpr (KV) vc[pos] = vs[j];
+                }
+            }
+            csync();
+            load_leaf(P, nxt, xs, vs);  // the next leaf's loads fly while this one is insertion-sorted and stored
+            // insertion sort of this thread's run (elements only move inside their bucket); `top` is
+            // the largest element of the sorted prefix, so an element already in place costs one compare
+            if (PDQ_KB_SKIP != 1 && r1 > r0) {  // (PDQ_KB_SKIP=1: profiling build, no insertion)
+                U top = kc[r0];
+                uint32_t vtop = KV ? vc[r0] : 0u;
+                for (int i = r0 + 1; i < r1; ++i) {
+                    const U x = kc[i];
+                    const uint32_t v = KV ? vc[i] : 0u;
+                    bool before = x < top;
+                    if constexpr (KV) before |= (x == top) && v < vtop;
+                    if (!before) {
+                        top = x;
+                        vtop = v;
+                        continue;
+                    }
+                    kc[i] = top;
+                    if (KV) vc[i] = vtop;
+                    int j = i - 1;
+                    for (; j > r0; --j) {
+                        const U y = kc[j - 1];
+                        bool gt = y > x;
+                        if constexpr (KV) gt |= (y == x) && vc[j - 1] > v;
+                        if (!gt) break;
+                        kc[j] = y;
+                        if (KV) vc[j] = vc[j - 1];
+                    }
+                    kc[j] = x;
+                    if (KV) vc[j] = v;
+                }
+            }
+            c = 1;
+        } else {
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) {
+                const int i = j * THREADS + tid;
+                if (j < J && i < m) {
+                    BB::kx()[i] = xs[j];
+                    if constexpr (KV) BB::vx()[i] = vs[j];
+                }
+            }
+            csync();
+            c = PDQ_KB_SKIP == 2 ? 0 : radix_leaf(m, mn, range, vmn, vmx);
+            load_leaf(P, nxt, xs, vs);  // (after the call: nothing of the leaf loop lives across it)
         }
         csync();
-        const U *fk = bufk[c];
+        const U *fk = kbuf(c);
         store_run<U>((U *)P.a_keys + b, m, [&](int i) { return O::from(fk[i]); });
         if (KV) {
-            const uint32_t *fv = bufv[c];
+            const uint32_t *fv = vbuf(c);
             store_run<uint32_t>(P.a_vals + b, m, [&](int i) { return fv[i]; });
         }
         csync();
@@ -490,6 +690,9 @@ struct Sorter {
             sh.s_base++;
             sh.s_bytes += 2ull * ELEM_BYTES * m;
             sh.s_cyc_base += clock64() - c0;
+        }
+        cur = nxt;
+        k ^= 1;
         }
         csync();
     }
@@ -1307,22 +1510,23 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
 }
 
 // ---- K7: the base-case kernel: persistent CTAs sort the queued leaves ---------------------------------
+#ifndef PDQ_BASE_MINB
+#define PDQ_BASE_MINB 4
+#endif
+// 4 CTAs/SM leave 64 registers per thread: the leaf's 16 keys per thread stay in registers
+template <class U, bool KV>
+constexpr int base_min_blocks() {
+    constexpr int fit = (228 * 1024) / (BaseBufs<U, KV>::bytes() + 2304);  // + static smem + reserve
+    return fit < PDQ_BASE_MINB ? (fit < 1 ? 1 : fit) : PDQ_BASE_MINB;
+}
 template <class U, bool FLOAT, bool KV>
-__global__ void __launch_bounds__(THREADS, BaseBufs<U, KV>::bytes() <= 45 * 1024 ? 5 : 2) k_base(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(THREADS, base_min_blocks<U, KV>()) k_base(const __grid_constant__ Params P) {
     using S = Sorter<U, FLOAT, KV>;
     Shared &sh = g_sh;
     const int tid = threadIdx.x;
     if (ld_volatile_u32(&P.st->reverse)) return;
     if (tid == 0) S::zero_counters();
-    const unsigned long long count = *(volatile unsigned long long *)&P.st->leaf_count;
-    for (;;) {
-        if (tid == 0) sh.npos = atomicAdd(&P.st->leaf_next, 1ull);
-        csync();
-        const unsigned long long idx = sh.npos;
-        if (idx >= count || idx >= P.leaf_cap) break;
-        const uint64_t lf = P.leaves[idx];
-        S::base_case(P, lf & 1u, (int64_t)(lf >> 14), (int)((lf >> 1) & 0x1FFF) + 1);
-    }
+    S::leaf_loop(P);
     csync();
     if (tid == 0) {
         atomicAdd(&P.st->c_bytes_base, sh.s_bytes);

@@ -9,6 +9,8 @@ import sys
 from collections import defaultdict
 
 rep = sys.argv[1]
+SORTKEY = "Instructions Executed" if "--by-inst" in sys.argv else "Warp Stall Sampling (All Samples)"
+sys.argv = [a for a in sys.argv if a != "--by-inst"]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
@@ -47,7 +49,7 @@ for r in rows:
 tot_s = sum(d["Warp Stall Sampling (All Samples)"] for d in agg.values()) or 1
 tot_i = sum(d["Instructions Executed"] for d in agg.values()) or 1
 print(f"total samples {tot_s}  warp-instructions {tot_i:.3g}")
-for key, d in sorted(agg.items(), key=lambda kv: -kv[1]["Warp Stall Sampling (All Samples)"])[:top]:
+for key, d in sorted(agg.items(), key=lambda kv: -kv[1][SORTKEY])[:top]:
     st = sorted(((v, k[6:]) for k, v in d.items() if k.startswith("stall_")), reverse=True)[:3]
     sts = " ".join(f"{k}:{v / max(1, d['Warp Stall Sampling (All Samples)']):.2f}" for v, k in st if v)
     print(f"{d['Warp Stall Sampling (All Samples)'] / tot_s:6.3f} inst {d['Instructions Executed'] / tot_i:6.3f} "

@@ -44,7 +44,7 @@ for r in range(reps):
           f"tiles {st['tiles']} base_cases {st['base_cases']}", flush=True)
 
 # per-level throughput: stop at depth d (profiling knob, output unsorted)
-if len(sys.argv) > 4:
+if len(sys.argv) > 4 and sys.argv[4]:
     from paper_2106_05123_b200 import SortConfig
     for d in [int(t) for t in sys.argv[4].split(",")]:
         ds2 = DeviceSorter(n, dt, kv)
