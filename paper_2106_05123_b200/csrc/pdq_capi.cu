@@ -243,12 +243,17 @@ extern "C" int pdq_sort_ex(void *keys, int dtype, uint32_t *payload, int64_t n, 
 
 
     const bool kv = payload != nullptr;
+#ifdef PDQ_ONLY_I32  // profiling builds (tools/): int32 keys-only instantiation, fast to compile
+    if (dtype == PDQ_I32 && !kv) return launch<uint32_t, false, false>(P, s, L, ev0, ev1);
+    return set_err(PDQ_ERR_DTYPE, "this profiling build sorts int32 keys only%s");
+#else
     switch (dtype) {
         case PDQ_I32: return kv ? launch<uint32_t, false, true>(P, s, L, ev0, ev1) : launch<uint32_t, false, false>(P, s, L, ev0, ev1);
         case PDQ_F32: return kv ? launch<uint32_t, true, true>(P, s, L, ev0, ev1) : launch<uint32_t, true, false>(P, s, L, ev0, ev1);
         case PDQ_I64: return kv ? launch<uint64_t, false, true>(P, s, L, ev0, ev1) : launch<uint64_t, false, false>(P, s, L, ev0, ev1);
         case PDQ_F64: return kv ? launch<uint64_t, true, true>(P, s, L, ev0, ev1) : launch<uint64_t, true, false>(P, s, L, ev0, ev1);
     }
+#endif
     return set_err(PDQ_ERR_DTYPE, "unsupported dtype code%s");
 }
 

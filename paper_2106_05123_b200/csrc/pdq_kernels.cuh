@@ -81,6 +81,7 @@ struct Shared {
     uint32_t ltile;          // next tile index to load within that task
     int wl[WARPS], weq[WARPS];
     long long L, R, lOff, rOff, fL, fE;
+    int aL, aR;  // kc positions of the current tile's left / right runs
     unsigned long long push_pos;
     uint32_t new_sid;
     int last;
@@ -111,10 +112,13 @@ __device__ __forceinline__ uint32_t mix32(uint64_t x) {
 // Dynamic shared memory of the persistent sorter: NST TMA stages and the compaction buffer kc
 // (keys, then payloads for KV).  Every pointer is computed arithmetically from the extern shared
 // symbol so the compiler emits LDS/STS, never generic LD/ST.
+// kc holds a tile's left and right runs, each placed at the 16-byte phase of its global destination
+// (so the run bodies leave by TMA bulk stores): up to KC_PAD elements of slack.
+constexpr int KC_PAD = 16;
 template <class U, bool KV>
 struct Bufs {
-    static constexpr int KEY_BYTES = (NST + 1) * TILE * (int)sizeof(U);
-    static constexpr int VAL_BYTES = KV ? (NST + 1) * TILE * 4 : 0;
+    static constexpr int KEY_BYTES = ((NST + 1) * TILE + KC_PAD) * (int)sizeof(U);
+    static constexpr int VAL_BYTES = KV ? ((NST + 1) * TILE + KC_PAD) * 4 : 0;
     __device__ __forceinline__ static U *stage(int i) { return reinterpret_cast<U *>(g_dsm) + i * TILE; }
     __device__ __forceinline__ static U *kc() { return reinterpret_cast<U *>(g_dsm) + NST * TILE; }
     __device__ __forceinline__ static uint32_t *vstage(int i) {
@@ -680,10 +684,10 @@ struct Sorter {
         }
         csync();
         const U *fk = kbuf(c);
-        store_run<U>((U *)P.a_keys + b, m, [&](int i) { return O::from(fk[i]); });
+        store_lin<U>((U *)P.a_keys + b, m, [&](int i) { return O::from(fk[i]); });
         if (KV) {
             const uint32_t *fv = vbuf(c);
-            store_run<uint32_t>(P.a_vals + b, m, [&](int i) { return fv[i]; });
+            store_lin<uint32_t>(P.a_vals + b, m, [&](int i) { return fv[i]; });
         }
         csync();
         if (tid == 0) {
@@ -1163,11 +1167,16 @@ struct Sorter {
         if (FULL) vmask = (1u << ITEMS) - 1;
     }
 
-    // Branch-free compaction of this thread's keys into kc: lefts from li, rights from ri.
+    // Branch-free compaction of this warp's keys into kc: its lefts fill [li, ...), its rights
+    // [ri, ...).  Ranks come from one ballot per item slot, so the 32 lanes of every store land in
+    // two contiguous runs of kc (at most a 2-way bank conflict; a per-thread prefix would put
+    // lanes ~8 words apart, an 8-way conflict).  Order within a side is free (no stability,
+    // PAPER.md:28-29).
     template <bool FULL>
     __device__ __forceinline__ static void scatter(const U *sk, const uint32_t *sv, U *kc, uint32_t *vc,
                                                    unsigned lmask, unsigned vmask, int li, int ri) {
         const int tid = threadIdx.x;
+        const unsigned ltm = lanemask_lt();
 #pragma unroll
         for (int jj = 0; jj < ITEMS / VEC; ++jj) {
             const int q = jj * THREADS + tid;
@@ -1178,28 +1187,65 @@ struct Sorter {
                 const int r = jj * VEC + e;
                 const bool isl = (lmask >> r) & 1u;
                 const bool valid = FULL || ((vmask >> r) & 1u);
-                const int pos = isl ? li : ri;
+                const unsigned bl = __ballot_sync(0xffffffffu, isl);
+                const unsigned br = FULL ? ~bl : __ballot_sync(0xffffffffu, valid && !isl);
+                const int pos = isl ? li + __popc(bl & ltm) : ri + __popc(br & ltm);
                 if (valid) {
                     kc[pos] = kk[e];
                     if (KV) vc[pos] = sv[q * VEC + e];
                 }
-                li += isl;
-                ri += valid && !isl;
+                li += __popc(bl);
+                ri += __popc(br);
             }
         }
+    }
+
+    // Store the run kc[a, a + len) (and vc) to dk[g, g + len) (and dv), a = g mod AL: the 16-byte
+    // aligned body by one TMA bulk store per array (issued by thread 0, committed by the caller),
+    // the < AL-element head and tail by threads t0 + i.
+    __device__ __forceinline__ static void emit_run(U *dk, uint32_t *dv, long long g, int a, int len, int t0) {
+        const int tid = threadIdx.x;
+        const U *kc = B::kc();
+        const uint32_t *vc = KV ? B::vc() : nullptr;
+        int h = (int)((AL - (g & (AL - 1))) & (AL - 1));
+        if (h > len) h = len;
+        const int nb = ((len - h) / AL) * AL;
+        const int i = tid - t0;
+        if (i >= 0 && i < AL) {
+            if (i < h) {
+                dk[g + i] = kc[a + i];
+                if (KV) dv[g + i] = vc[a + i];
+            }
+            const int j = h + nb + i;
+            if (j < len) {
+                dk[g + j] = kc[a + j];
+                if (KV) dv[g + j] = vc[a + j];
+            }
+        }
+        if (tid == 0 && nb) {
+            bulk_s2g(dk + g + h, kc + a + h, (unsigned)(nb * sizeof(U)));
+            if (KV) bulk_s2g(dv + g + h, vc + a + h, (unsigned)(nb * 4));
+        }
+    }
+
+    // Contiguous coalesced store of `len` elements of shared memory run `s` to global `g`: lane
+    // stride 1 on both sides (conflict-free shared reads; alignment of g is arbitrary).
+    template <class T, class F>
+    __device__ __forceinline__ static void store_lin(T *g, int len, F get) {
+        for (int i = threadIdx.x; i < len; i += THREADS) g[i] = get(i);
     }
 
     // Partition the tile in stage `s`; returns after the stores are issued.  Releases the stage
     // (empty barrier) as soon as its buffer has been consumed.
     //   left = key <  pivot  (partition_right: equals go right, partition.py:76-77)
     //   left = key <= pivot  (partition_left: equals go left, partition.py:134-135)
-    // Each thread counts its own keys; one block-wide exclusive scan (packed left|right<<16)
-    // gives every thread its slots in the compaction buffer: lefts fill kc from the front,
-    // rights follow them.  One 64-bit atomic per CTA reserves both output runs.
+    // Each warp sums its counts; the per-warp totals (packed left | right << 16) give every warp its
+    // runs in the compaction buffer kc.  One 64-bit atomic per CTA reserves both output runs before
+    // the scatter, so each run is placed in kc at the 16-byte phase of its destination and its body
+    // leaves by one TMA bulk store (no per-key store instructions).
     // One partition tile of the current task (sh.seg), whose TMA load is in flight in the stage.
     // After the stage is consumed thread 0 starts the next load (next tile of this chunk, or the
-    // first tile of the already-claimed next task), so the load overlaps this tile's reservation
-    // atomic and stores.
+    // first tile of the already-claimed next task), so the load overlaps this tile's stores.
     __device__ static void part_tile(const Params &P, uint32_t sid, uint32_t tile, unsigned &ci) {
         Shared &sh = g_sh;
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1231,15 +1277,10 @@ struct Sorter {
             classify<false>(sk, sv, lo_i, hi_i, piv, pv, left_mode, count_eq, lmask, vmask, eqc);
         const int nl = __popc(lmask), nv = __popc(vmask);
         const uint32_t mine = (uint32_t)nl | ((uint32_t)(nv - nl) << 16);
-        uint32_t inc = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
+        const uint32_t wsum = __reduce_add_sync(0xffffffffu, mine);  // warp totals, left | right << 16
         if (count_eq) eqc = __reduce_add_sync(0xffffffffu, eqc);
-        if (lane == 31) {
-            sh.scan[warp] = inc;
+        if (lane == 0) {
+            sh.scan[warp] = wsum;
             sh.weq[warp] = eqc;
         }
         csync();
@@ -1251,16 +1292,20 @@ struct Sorter {
             tot += x;
         }
         const int L = (int)(tot & 0xFFFF), R = (int)(tot >> 16);
-        unsigned long long res_lr = 0, res_r = 0;
+        const bool write_left = !left_mode || srcB;  // K3 from A: the lefts are filled later
         if (tid == 0) {
             // one atomic per CTA reserves both runs (left grows up from `begin`, right grows down
-            // from `end`); its result is consumed only after the scatter below
+            // from `end`); the runs are placed in kc at the 16-byte phase of their destinations
             Seg *gs = &P.segs[sid];
+            long long lOff, rOff;
             if (packed) {
-                res_lr = atomicAdd(&gs->cnt_left, (unsigned long long)L | ((unsigned long long)R << 32));
+                const unsigned long long r =
+                    atomicAdd(&gs->cnt_left, (unsigned long long)L | ((unsigned long long)R << 32));
+                lOff = (long long)(r & 0xFFFFFFFFull);
+                rOff = (long long)(r >> 32);
             } else {
-                res_lr = atomicAdd(&gs->cnt_left, (unsigned long long)L);
-                res_r = atomicAdd(&gs->cnt_right, (unsigned long long)R);
+                lOff = (long long)atomicAdd(&gs->cnt_left, (unsigned long long)L);
+                rOff = (long long)atomicAdd(&gs->cnt_right, (unsigned long long)R);
             }
             if (count_eq) {
                 int E = 0;
@@ -1268,45 +1313,39 @@ struct Sorter {
                 for (int w = 0; w < WARPS; ++w) E += sh.weq[w];
                 if (E) atomicAdd(&gs->cnt_eq, (unsigned long long)E);
             }
+            const long long gl = b + lOff, gr = e - rOff - R;
+            const int aL = (int)(gl & (AL - 1));
+            const int aR = aL + L + (int)((gr - (aL + L)) & (AL - 1));
+            sh.lOff = gl;
+            sh.rOff = gr;
+            sh.aL = aL;
+            sh.aR = aR;
+            sh.s_tiles++;
+            sh.s_bytes += (unsigned long long)ELEM_BYTES * (L + R) +
+                          (unsigned long long)ELEM_BYTES * (R + (write_left ? L : 0));
+            bulk_wait_read();  // the previous tile's bulk stores have left kc
         }
-        const uint32_t pre = wpre + inc - mine;
-        const int li0 = (int)(pre & 0xFFFF), ri0 = L + (int)(pre >> 16);
+        csync();
+        const int aL = sh.aL, aR = sh.aR;
+        const int li0 = aL + (int)(wpre & 0xFFFF), ri0 = aR + (int)(wpre >> 16);  // this warp's runs in kc
         U *kc = B::kc();
         uint32_t *vc = KV ? B::vc() : nullptr;
-        if (vmask == (1u << ITEMS) - 1)
+        if (lo_i == 0 && hi_i == TILE)  // CTA-uniform (the ballots need every lane)
             scatter<true>(sk, sv, kc, vc, lmask, vmask, li0, ri0);
         else
             scatter<false>(sk, sv, kc, vc, lmask, vmask, li0, ri0);
-        csync();  // stage consumed
+        fence_proxy_async();  // kc (generic writes) is read next by the TMA engine
+        csync();              // stage consumed, kc complete
+        const long long gl = sh.lOff, gr = sh.rOff;
+        U *dst = (U *)(srcB ? P.a_keys : P.b_keys);
+        uint32_t *dstv = srcB ? P.a_vals : P.b_vals;
         if (tid == 0) {
             sh.ci = ci;
             pump_loads(P);
-            const long long q2 = clock64();
-            if (packed) {
-                sh.lOff = (long long)(res_lr & 0xFFFFFFFFull);
-                sh.rOff = (long long)(res_lr >> 32);
-            } else {
-                sh.lOff = (long long)res_lr;
-                sh.rOff = (long long)res_r;
-            }
-            sh.s_sch_fetch += clock64() - q2;  // (profiling) wait for the reservation atomic
-            sh.s_tiles++;
-            const bool write_left = !left_mode || srcB;
-            sh.s_bytes += (unsigned long long)ELEM_BYTES * (L + R) +
-                          (unsigned long long)ELEM_BYTES * (R + (write_left ? L : 0));
         }
-        csync();
-        const long long lOff = sh.lOff, rOff = sh.rOff;
-        U *dst = (U *)(srcB ? P.a_keys : P.b_keys);
-        uint32_t *dstv = srcB ? P.a_vals : P.b_vals;
-        if (L && (!left_mode || srcB)) {
-            store_run<U>(dst + b + lOff, L, [&](int i) { return kc[i]; });
-            if (KV) store_run<uint32_t>(dstv + b + lOff, L, [&](int i) { return vc[i]; });
-        }
-        if (R) {
-            store_run<U>(dst + e - rOff - R, R, [&](int i) { return kc[L + i]; });
-            if (KV) store_run<uint32_t>(dstv + e - rOff - R, R, [&](int i) { return vc[L + i]; });
-        }
+        if (L && write_left) emit_run(dst, dstv, gl, aL, L, 0);
+        if (R) emit_run(dst, dstv, gr, aR, R, 64);
+        if (tid == 0) bulk_commit();
         if (tid == 0) sh.s_sch_idle += clock64() - q1;  // (profiling) whole tile after the stage wait
     }
 
@@ -1351,6 +1390,7 @@ struct Sorter {
             for (int q = 0; q < 8; ++q) sdst[q] = __ldcg(gsrc + q);
             sh.ntask = w;
             sh.nstate = 2;
+            fence_proxy_async_global();  // the task's data (acquired above) is read by TMA bulk loads
         }
     }
 
@@ -1592,7 +1632,12 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
             const uint32_t t0 = ((uint32_t)w & 0x7FFFFF) * CHUNK;
             const uint32_t t1 = min(t0 + CHUNK, sh.seg.ntiles);
             for (uint32_t t = t0; t < t1; ++t) S::part_tile(P, sid, t, ci);
-            // retire the chunk: one gpu-scope fence per thread, one counter update per CTA
+            // retire the chunk: the bulk stores complete, one gpu-scope fence per thread, one
+            // counter update per CTA
+            if (tid == 0) {
+                bulk_wait_all();
+                fence_proxy_async_global();
+            }
             __threadfence();
             csync();
             if (tid == 0) {
