@@ -34,7 +34,7 @@ extern "C" void pdq_config_default(pdq_config *c) {
     c->use_partition_left = 1;
     c->use_break_patterns = 1;
     c->use_partial_insertion = 1;
-    c->base_case_size = MAX_BASE;
+    c->base_case_size = BIG_BASE;
     c->bad_budget = -1;
 }
 
@@ -49,8 +49,8 @@ extern "C" int pdq_config_validate(const pdq_config *c) {
     if (c->block_size < 1) return set_err(PDQ_ERR_CONFIG, "block_size must be >= 1%s");
     if (c->bad_partition_shift < 1) return set_err(PDQ_ERR_CONFIG, "bad_partition_shift must be >= 1%s");
     if (c->bad_partition_shift > 62) return set_err(PDQ_ERR_CONFIG, "bad_partition_shift must be <= 62%s");
-    if (c->base_case_size < 1024 || c->base_case_size > MAX_BASE)
-        return set_err(PDQ_ERR_CONFIG, "base_case_size must be in [1024, 4096]%s");
+    if (c->base_case_size < 1024 || c->base_case_size > BIG_BASE)
+        return set_err(PDQ_ERR_CONFIG, "base_case_size must be in [1024, 16384]%s");
     return PDQ_OK;
 }
 
@@ -114,6 +114,12 @@ struct LaunchInfo {
     int occ_base = 0;
 };
 
+// 4-byte keys without payload: 16K-key leaves sorted by k_base_big; other elements: 4K leaves (k_base)
+template <class U, bool KV>
+constexpr bool big_leaves() {
+    return sizeof(U) == 4 && !KV;
+}
+
 template <class U, bool FLOAT, bool KV>
 int smem_bytes() {
     return Bufs<U, KV>::bytes();
@@ -136,13 +142,20 @@ cudaError_t prepare(LaunchInfo &li) {
         if ((e = cudaFuncSetAttribute(k_init<U, FLOAT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) !=
             cudaSuccess)
             return e;
-        const int smb = BaseBufs<U, KV>::bytes();
-        if ((e = cudaFuncSetAttribute(k_base<U, FLOAT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb)) !=
-            cudaSuccess)
-            return e;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached.occ_base, k_base<U, FLOAT, KV>, THREADS, smb)) !=
-            cudaSuccess)
-            return e;
+        if constexpr (big_leaves<U, KV>()) {
+            if ((e = cudaFuncSetAttribute(k_base_big<FLOAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          BigLeaf<FLOAT>::bytes())) != cudaSuccess)
+                return e;
+            cached.occ_base = 1;
+        } else {
+            const int smb = BaseBufs<U, KV>::bytes();
+            if ((e = cudaFuncSetAttribute(k_base<U, FLOAT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb)) !=
+                cudaSuccess)
+                return e;
+            if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached.occ_base, k_base<U, FLOAT, KV>, THREADS,
+                                                                   smb)) != cudaSuccess)
+                return e;
+        }
         if (cached.occ_base < 1) cached.occ_base = 1;
         if ((e = cudaDeviceGetAttribute(&cached.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached.occ, k_sort<U, FLOAT, KV>, THREADS, sm)) !=
@@ -158,6 +171,8 @@ cudaError_t prepare(LaunchInfo &li) {
 template <class U, bool FLOAT, bool KV>
 int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEvent_t ev1) {
     LaunchInfo li;
+    const int base_max = big_leaves<U, KV>() ? BIG_BASE : MAX_BASE;
+    if (P.base_size > base_max) P.base_size = base_max;
     cudaError_t e = prepare<U, FLOAT, KV>(li);
     if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "setup: %s", cudaGetErrorString(e));
     const int sm = smem_bytes<U, FLOAT, KV>();
@@ -172,7 +187,10 @@ int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEven
     if (ev0) cudaEventRecord(ev0, s);
     k_sort<U, FLOAT, KV><<<(unsigned)(li.sms * li.occ), THREADS, sm, s>>>(P);
     if (ev1) cudaEventRecord(ev1, s);
-    k_base<U, FLOAT, KV><<<(unsigned)(li.sms * li.occ_base), THREADS, BaseBufs<U, KV>::bytes(), s>>>(P);
+    if constexpr (big_leaves<U, KV>())
+        k_base_big<FLOAT><<<(unsigned)li.sms, BigLeaf<FLOAT>::BT, BigLeaf<FLOAT>::bytes(), s>>>(P);
+    else
+        k_base<U, FLOAT, KV><<<(unsigned)(li.sms * li.occ_base), THREADS, BaseBufs<U, KV>::bytes(), s>>>(P);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "launch: %s", cudaGetErrorString(e));
     return PDQ_OK;

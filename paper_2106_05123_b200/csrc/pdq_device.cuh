@@ -18,7 +18,8 @@ namespace pdq {
 constexpr int THREADS = 256;          // threads per CTA in every kernel
 constexpr int TILE = 4096;            // keys per partition tile (one "block" of partition.py:184)
 constexpr int ITEMS = TILE / THREADS; // keys per thread per tile
-constexpr int MAX_BASE = 4096;        // largest base-case segment (K7)
+constexpr int MAX_BASE = 4096;        // largest base-case segment (K7) for 8-byte and KV elements
+constexpr int BIG_BASE = 16384;       // largest base-case segment for 4-byte keys-only sorts (k_base_big)
 constexpr int SAMPLES = 256;          // K1 pivot samples per big segment
 constexpr int WARPS = THREADS / 32;
 constexpr int64_t INLINE_FILL = 16 * TILE;  // fills up to this size run inline in the finalizer
@@ -109,7 +110,7 @@ struct Params {
     int base_size;
     int budget0;
     int debug_depth;   // > 0: segments at this depth are dropped unsorted (profiling only)
-    uint64_t *leaves;  // queued leaves: begin << 14 | (size - 1) << 1 | in-B
+    uint64_t *leaves;  // queued leaves: begin << 16 | (size - 1) << 1 | in-B
     unsigned long long leaf_cap;
 };
 

@@ -449,8 +449,8 @@ struct Sorter {
     __device__ __forceinline__ static void load_leaf(const Params &P, uint64_t lf, U (&xs)[ITEMS],
                                                      uint32_t (&vs)[KV ? ITEMS : 1]) {
         const int tid = threadIdx.x;
-        const int m = lf == ~0ull ? 0 : (int)((lf >> 1) & 0x1FFF) + 1;
-        const int64_t b = (int64_t)(lf >> 14);
+        const int m = lf == ~0ull ? 0 : (int)((lf >> 1) & 0x7FFF) + 1;
+        const int64_t b = (int64_t)(lf >> 16);
         const U *src = (const U *)((lf & 1u) ? P.b_keys : P.a_keys);
         const uint32_t *srcv = (lf & 1u) ? P.b_vals : P.a_vals;
 #pragma unroll
@@ -497,8 +497,8 @@ struct Sorter {
         while (cur != NONE) {
         const long long c0 = clock64();
         claim(k ^ 1);
-        const int m = (int)((cur >> 1) & 0x1FFF) + 1;
-        const int64_t b = (int64_t)(cur >> 14);
+        const int m = (int)((cur >> 1) & 0x7FFF) + 1;
+        const int64_t b = (int64_t)(cur >> 16);
         const int J = (m + THREADS - 1) / THREADS;
         {  // zero the bucket counters while the loads are in flight
             uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
@@ -886,7 +886,7 @@ struct Sorter {
             } else if (tid == 0) {
                 const unsigned long long pos = atomicAdd(&P.st->leaf_count, 1ull);
                 if (pos < P.leaf_cap)
-                    P.leaves[pos] = (uint64_t)b << 14 | (uint64_t)(m - 1) << 1 | (srcB ? 1u : 0u);
+                    P.leaves[pos] = (uint64_t)b << 16 | (uint64_t)(m - 1) << 1 | (srcB ? 1u : 0u);
                 else
                     fail(P, -6);
                 finish_keys(P, (unsigned long long)m);
@@ -1547,6 +1547,401 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
     }
     __syncthreads();
     if (tid == 0) S::flush_counters(P);
+}
+
+// ---- K7 for 4-byte keys-only sorts: leaves of up to BIG_BASE = 16384 keys -----------------------------
+// One CTA of 1024 threads per SM; a leaf lives in registers (16 keys per thread) while it is bucketed:
+//   1. ordered image, block min/max; a constant leaf is already sorted (copied to A if it is in B);
+//   2. bucket(x) = hi32(((x - min) << clz(range)) * F), a monotone map onto 8192 buckets; a shared-memory
+//      atomic gives every key its slot, one block scan turns counts into (start, count) words;
+//   3. keys go to kc[start + slot]; a key whose bucket holds other keys is ranked among them (number
+//      of smaller keys, ties by slot), every other key keeps its slot; the result goes to kd at the
+//      16-byte phase of the leaf's place in A and leaves by one TMA bulk store.
+// A leaf with a bucket larger than CMAX takes the slow path: such a bucket is accepted if it is
+// constant (repeated keys), otherwise the leaf is sorted by stable 8-bit LSD radix passes over
+// (key - min).  On the fast path the next leaf's loads fly while the current one is ranked.
+// Replaces insertion_sort / unguarded_insertion_sort (small_sorts.py:16-73) with a 16K-key leaf, which
+// removes the two deepest partition levels of a 2^28-key sort.
+#ifndef PDQ_BIG_SKIP
+#define PDQ_BIG_SKIP 0  // profiling builds only: 1 = no in-bucket ranking (output NOT sorted)
+#endif
+template <bool FLOAT>
+struct BigLeaf {
+    using U = uint32_t;
+    using O = Ord<U, FLOAT>;
+    static constexpr int BT = 1024, BW = BT / 32, BI = BIG_BASE / BT;
+#ifndef PDQ_BIG_LOGBK
+#define PDQ_BIG_LOGBK 13
+#endif
+    static constexpr int LOG_BK = PDQ_BIG_LOGBK, BBK = 1 << LOG_BK;  // buckets
+    static constexpr int CMAX = 32;                       // largest bucket ranked by comparisons
+    static constexpr int KD_OFF = BIG_BASE, CNT_OFF = KD_OFF + BIG_BASE + 16, RED_OFF = CNT_OFF + BBK,
+                         WORDS = RED_OFF + 128;
+    __host__ __device__ static constexpr int bytes() { return WORDS * 4; }
+    __device__ __forceinline__ static uint32_t *wd() { return reinterpret_cast<uint32_t *>(g_dsm); }
+    __device__ __forceinline__ static void bsync() { asm volatile("bar.sync 1, %0;" ::"n"(BT) : "memory"); }
+    __device__ __forceinline__ static int bsync_or(int p) {
+        int r;
+        asm volatile(
+            "{\n .reg .pred a, b;\n setp.ne.s32 a, %1, 0;\n bar.red.or.pred b, 1, %2, a;\n selp.s32 %0, 1, 0, b;\n}\n"
+            : "=r"(r)
+            : "r"(p), "n"(BT)
+            : "memory");
+        return r;
+    }
+    __device__ __forceinline__ static uint32_t warp_incl_scan(uint32_t v) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        return v;
+    }
+    // exclusive block scan of one value per thread, and the block max of `mx` (red[0, 64) scratch;
+    // contains a barrier)
+    __device__ __forceinline__ static uint32_t block_excl_scan(uint32_t v, uint32_t *red, uint32_t mx = 0,
+                                                               uint32_t *bmax = nullptr) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const uint32_t inc = warp_incl_scan(v);
+        if (bmax) mx = __reduce_max_sync(0xffffffffu, mx);
+        if (lane == 31) red[warp] = inc;
+        if (bmax && lane == 0) red[32 + warp] = mx;
+        bsync();
+        const uint32_t t = warp_incl_scan(red[lane]);
+        if (bmax) *bmax = __reduce_max_sync(0xffffffffu, red[32 + lane]);
+        const uint32_t wpre = __shfl_sync(0xffffffffu, t, (warp + 31) & 31);
+        return (warp ? wpre : 0u) + inc - v;
+    }
+
+    __device__ __forceinline__ static void load(const Params &P, uint64_t lf, U (&xs)[BI]) {
+        const int tid = threadIdx.x;
+        const int m = lf == ~0ull ? 0 : (int)((lf >> 1) & 0x7FFF) + 1;
+        const int64_t b = (int64_t)(lf >> 16);
+        const U *src = (const U *)((lf & 1u) ? P.b_keys : P.a_keys);
+#pragma unroll
+        for (int j = 0; j < BI; ++j) {
+            const int i = j * BT + tid;
+            xs[j] = i < m ? ldcg(src + b + i) : 0u;
+        }
+    }
+
+    // the monotone bucket map of a leaf: hi32(((x - mn) << sh) * F)
+    struct Map {
+        U mn;
+        int sh;
+        uint32_t F;
+        __device__ __forceinline__ uint32_t operator()(U x) const { return __umulhi((x - mn) << sh, F); }
+    };
+    __device__ __forceinline__ static Map make_map(U mn, U range) {
+        Map mp;
+        mp.mn = mn;
+        mp.sh = __clz(range);                 // range > 0
+        const uint32_t ymax = range << mp.sh;  // in [2^31, 2^32)
+        // F <= 2^(32 + LOG_BK) / (ymax + 1) keeps every bucket below BBK (the float quotient is at most
+        // one unit high; the subtraction makes it safe)
+        mp.F = (uint32_t)__fdividef((float)(1ull << (32 + LOG_BK)), (float)ymax + 1.0f) - 2u;
+        return mp;
+    }
+
+    // rank of key x (at slot position p of kc) inside its bucket (start | count << 16)
+    __device__ __forceinline__ static uint32_t rank_in_bucket(const uint32_t *kc, U x, uint32_t p, uint32_t sc) {
+        const uint32_t s0 = sc & 0xFFFFu, c = sc >> 16;
+        if (PDQ_BIG_SKIP || c <= 1) return p;
+        // four independent loads per step (the bucket's neighbours beyond s0 + c are read but not counted)
+        uint32_t r = s0;
+        const uint32_t e = s0 + c;
+        for (uint32_t i = s0; i < e; i += 4) {
+            U y[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) y[q] = kc[i + q];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) r += (i + q < e) & ((y[q] < x) | ((y[q] == x) & (i + q < p)));
+        }
+        return r;
+    }
+
+    // One stable 8-bit counting pass src -> dst over ((x - mn) >> shift) & 255 (ordered images); the
+    // final pass writes raw keys.  Warp w owns elements [512w, 512w + 512) in 16 rounds of 32; ranks
+    // within a warp from a ballot multisplit, per-warp 16-bit digit counters, one digit-major block scan.
+    __device__ __forceinline__ static void radix_pass(const uint32_t *src, uint32_t *dst, int m, U mn, int shift,
+                                                      bool fin) {
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        uint16_t *wc16 = reinterpret_cast<uint16_t *>(wd() + CNT_OFF);
+        uint16_t *wc = wc16 + warp * 256;
+        uint32_t *red = wd() + RED_OFF;
+        reinterpret_cast<uint4 *>(wc)[lane] = make_uint4(0u, 0u, 0u, 0u);  // 256 counters
+        __syncwarp();
+        const unsigned ltm = lanemask_lt();
+        uint32_t rd[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int idx = warp * 512 + j * 32 + lane;
+            const bool valid = idx < m;
+            const uint32_t d = valid ? ((src[idx] - mn) >> shift) & 255u : 0u;
+            unsigned peers = __ballot_sync(0xffffffffu, valid);
+            peers = valid ? peers : ~peers;
+#pragma unroll
+            for (int bit = 0; bit < 8; ++bit) {
+                const bool on = (d >> bit) & 1u;
+                const unsigned bb = __ballot_sync(0xffffffffu, on);
+                peers &= on ? bb : ~bb;
+            }
+            const uint32_t before = valid ? (uint32_t)wc[d] : 0u;
+            const uint32_t r = (uint32_t)__popc(peers & ltm);
+            __syncwarp();
+            if (valid && r == 0) wc[d] = (uint16_t)(before + __popc(peers));
+            __syncwarp();
+            rd[j] = ((before + r) << 8) | d;
+        }
+        bsync();
+        // digit-major scan over (digit, warp): thread t owns digit t >> 2, warps 8 (t & 3) .. + 8
+        {
+            const int d = tid >> 2, w0 = 8 * (tid & 3);
+            uint32_t c[8], tot = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                c[q] = wc16[(w0 + q) * 256 + d];
+                tot += c[q];
+            }
+            uint32_t run = block_excl_scan(tot, red);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                wc16[(w0 + q) * 256 + d] = (uint16_t)run;
+                run += c[q];
+            }
+        }
+        bsync();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int idx = warp * 512 + j * 32 + lane;
+            if (idx < m) {
+                const uint32_t pos = (uint32_t)wc[rd[j] & 0xFFu] + (rd[j] >> 8);
+                const U x = src[idx];
+                dst[pos] = fin ? O::from(x) : x;
+            }
+        }
+        bsync();
+    }
+
+    // Slow path (a bucket holds more than CMAX keys).  kc holds the bucketed leaf and cnt the
+    // (start, count) words; writes kd[a0 + i] = raw keys in order.
+    __device__ __noinline__ static void slow_leaf(int m, int a0, const Map mp, U range, const uint32_t (&pp)[BI / 2]) {
+        const int tid = threadIdx.x;
+        uint32_t *kc = wd(), *kd = wd() + KD_OFF, *cnt = wd() + CNT_OFF;
+        int fb = 0;
+#pragma unroll
+        for (int j = 0; j < BI; ++j) {
+            if (j * BT + tid < m) {
+                const uint32_t p = (pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu;
+                const U x = kc[p];
+                const uint32_t sc = cnt[mp(x)];
+                if ((sc >> 16) > (uint32_t)CMAX && kc[sc & 0xFFFFu] != x) fb = 1;  // a big mixed bucket
+            }
+        }
+        if (!bsync_or(fb)) {
+            // every big bucket is constant: its keys keep their slots, the others are ranked
+#pragma unroll
+            for (int j = 0; j < BI; ++j) {
+                if (j * BT + tid < m) {
+                    const uint32_t p = (pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu;
+                    const U x = kc[p];
+                    const uint32_t sc = cnt[mp(x)];
+                    const uint32_t r = (sc >> 16) > (uint32_t)CMAX ? p : rank_in_bucket(kc, x, p, sc);
+                    kd[a0 + r] = O::from(x);
+                }
+            }
+            return;
+        }
+        // clustered distinct keys: LSD radix passes over (key - mn); the final pass reads kc, writes kd
+        const int np = (32 - __clz(range) + 7) / 8;
+        const uint32_t *src = kc;
+        uint32_t *dst = kd;
+        if ((np & 1) == 0) {
+            for (int i = tid; i < m; i += BT) kd[i] = kc[i];
+            bsync();
+            src = kd;
+            dst = kc;
+        }
+        for (int q = 0; q < np; ++q) {
+            const bool fin = q == np - 1;
+            radix_pass(src, fin ? kd + a0 : dst, m, mp.mn, 8 * q, fin);
+            const uint32_t *t = src;
+            src = dst;
+            dst = const_cast<uint32_t *>(t);
+        }
+    }
+
+    __device__ static void run(const Params &P) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        uint32_t *kc = wd(), *kd = wd() + KD_OFF, *cnt = wd() + CNT_OFF, *red = wd() + RED_OFF;
+        unsigned long long count = *(volatile unsigned long long *)&P.st->leaf_count;
+        if (count > P.leaf_cap) count = P.leaf_cap;
+        constexpr uint64_t NONE = ~0ull;
+        auto claim = [&](int k) {
+            if (tid == 0) {
+                const unsigned long long idx = atomicAdd(&P.st->leaf_next, 1ull);
+                sh.lf[k] = idx < count ? ldcg(P.leaves + idx) : NONE;
+            }
+        };
+        U xs[BI];
+        claim(0);
+        bsync();
+        uint64_t cur = sh.lf[0];
+        int k = 0;
+        load(P, cur, xs);
+        while (cur != NONE) {
+            const long long c0 = clock64();
+            claim(k ^ 1);
+            const int m = (int)((cur >> 1) & 0x7FFF) + 1;
+            const int64_t b = (int64_t)(cur >> 16);
+            const bool srcB = cur & 1u;
+            {  // zero the bucket counters while the loads are in flight
+                uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
+#pragma unroll
+                for (int q = 0; q < BBK / 4 / BT; ++q) c4[q * BT + tid] = make_uint4(0, 0, 0, 0);
+            }
+            U mn = ~0u, mx = 0u;
+#pragma unroll
+            for (int j = 0; j < BI; ++j) {
+                if (j * BT + tid < m) {
+                    const U x = O::to(xs[j]);
+                    xs[j] = x;
+                    mn = min(mn, x);
+                    mx = max(mx, x);
+                }
+            }
+            mn = __reduce_min_sync(0xffffffffu, mn);
+            mx = __reduce_max_sync(0xffffffffu, mx);
+            if (lane == 0) {
+                red[64 + warp] = mn;
+                red[96 + warp] = mx;
+            }
+            bsync();
+            mn = __reduce_min_sync(0xffffffffu, red[64 + lane]);
+            mx = __reduce_max_sync(0xffffffffu, red[96 + lane]);
+            const uint64_t nxt = sh.lf[k ^ 1];  // written by thread 0 before the barrier above
+            const U range = mx - mn;
+            if (range == 0) {
+                // a constant leaf is sorted; one in B is copied to its place in A
+                if (srcB) {
+                    U *a = (U *)P.a_keys + b;
+#pragma unroll
+                    for (int j = 0; j < BI; ++j)
+                        if (j * BT + tid < m) a[j * BT + tid] = O::from(xs[j]);
+                }
+                load(P, nxt, xs);
+                if (tid == 0) {
+                    sh.s_base++;
+                    sh.s_bytes += (srcB ? 2ull : 1ull) * 4 * m;
+                    sh.s_cyc_base += clock64() - c0;
+                }
+                bsync();
+                cur = nxt;
+                k ^= 1;
+                continue;
+            }
+            const Map mp = make_map(mn, range);
+            uint32_t pp[BI / 2];  // 16-bit slots, then 16-bit positions in kc
+#pragma unroll
+            for (int j = 0; j < BI; ++j) {
+                const uint32_t sl = (j * BT + tid < m) ? atomicAdd(&cnt[mp(xs[j])], 1u) : 0u;
+                if (j & 1) pp[j / 2] |= sl << 16;
+                else pp[j / 2] = sl;
+            }
+            bsync();
+            uint32_t cmax;
+            {  // (start, count) words: thread t owns buckets [PB t, PB t + PB)
+                constexpr int PB = BBK / BT;
+                uint32_t cw[PB];
+                uint4 *c4 = reinterpret_cast<uint4 *>(cnt + PB * tid);
+#pragma unroll
+                for (int q = 0; q < PB / 4; ++q) {
+                    const uint4 y = c4[q];
+                    cw[4 * q] = y.x; cw[4 * q + 1] = y.y; cw[4 * q + 2] = y.z; cw[4 * q + 3] = y.w;
+                }
+                uint32_t tot = 0, mc = 0;
+#pragma unroll
+                for (int q = 0; q < PB; ++q) {
+                    tot += cw[q];
+                    mc = max(mc, cw[q]);
+                }
+                uint32_t run = block_excl_scan(tot, red, mc, &cmax);
+#pragma unroll
+                for (int q = 0; q < PB; ++q) {
+                    const uint32_t c = cw[q];
+                    cw[q] = run | (c << 16);
+                    run += c;
+                }
+#pragma unroll
+                for (int q = 0; q < PB / 4; ++q) c4[q] = make_uint4(cw[4 * q], cw[4 * q + 1], cw[4 * q + 2], cw[4 * q + 3]);
+            }
+            bsync();
+#pragma unroll
+            for (int j = 0; j < BI; ++j) {
+                if (j * BT + tid < m) {
+                    const uint32_t sh16 = (j & 1) << 4;
+                    const uint32_t p = (cnt[mp(xs[j])] & 0xFFFFu) + ((pp[j / 2] >> sh16) & 0xFFFFu);
+                    kc[p] = xs[j];
+                    pp[j / 2] = (pp[j / 2] & ~(0xFFFFu << sh16)) | (p << sh16);
+                }
+            }
+            const int a0 = (int)(b & 3);
+            if (tid == 0) bulk_wait_read();  // the previous leaf's bulk store has left kd
+            bsync();
+            if (cmax <= (uint32_t)CMAX) {
+                load(P, nxt, xs);  // the next leaf's loads fly while this one is ranked and stored
+#pragma unroll
+                for (int j = 0; j < BI; ++j) {
+                    if (j * BT + tid < m) {
+                        const uint32_t p = (pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu;
+                        const U x = kc[p];
+                        kd[a0 + rank_in_bucket(kc, x, p, cnt[mp(x)])] = O::from(x);
+                    }
+                }
+            } else {
+                slow_leaf(m, a0, mp, range, pp);
+                load(P, nxt, xs);
+            }
+            fence_proxy_async();
+            bsync();
+            {  // kd[a0, a0 + m) -> A[b, b + m): 16-byte body by one bulk store, head/tail by threads
+                U *a = (U *)P.a_keys + b;
+                int h = (4 - a0) & 3;
+                if (h > m) h = m;
+                const int nb = ((m - h) / 4) * 4;
+                if (tid > 0 && tid < 4 && tid - 1 < h) a[tid - 1] = kd[a0 + tid - 1];
+                if (tid >= 4 && tid < 8 && h + nb + tid - 4 < m) a[h + nb + tid - 4] = kd[a0 + h + nb + tid - 4];
+                if (tid == 0) {
+                    if (nb) bulk_s2g(a + h, kd + a0 + h, (unsigned)nb * 4u);
+                    bulk_commit();
+                    sh.s_base++;
+                    sh.s_bytes += 8ull * m;
+                    sh.s_cyc_base += clock64() - c0;
+                }
+            }
+            cur = nxt;
+            k ^= 1;
+        }
+        if (tid == 0) bulk_wait_all();
+        bsync();
+    }
+};
+
+template <bool FLOAT>
+__global__ void __launch_bounds__(BigLeaf<FLOAT>::BT, 1) k_base_big(const __grid_constant__ Params P) {
+    using S = Sorter<uint32_t, FLOAT, false>;
+    Shared &sh = g_sh;
+    const int tid = threadIdx.x;
+    if (ld_volatile_u32(&P.st->reverse)) return;
+    if (tid == 0) S::zero_counters();
+    BigLeaf<FLOAT>::run(P);
+    if (tid == 0) {
+        atomicAdd(&P.st->c_bytes_base, sh.s_bytes);
+        sh.s_bytes = 0;
+        S::flush_counters(P);
+    }
 }
 
 // ---- K7: the base-case kernel: persistent CTAs sort the queued leaves ---------------------------------

@@ -72,7 +72,7 @@ def shapes(n, rng, dtype):
 
 
 SWEEP_SIZES = list(range(0, 65)) + [100, 1000, 1023, 1024, 1025, 4095, 4096, 4097, 8191, 8192, 10007,
-                                     65536, 100003, 1 << 20]
+                                     16383, 16384, 16385, 32769, 65536, 100003, 1 << 20]
 
 
 @pytest.mark.parametrize("dtype", DTYPES, ids=lambda d: np.dtype(d).name)
@@ -182,7 +182,7 @@ def test_forced_fallback_budget_zero(dtype):
     # bad_budget=0: the root starts with an exhausted budget, so it takes the K5 radix split
     # (driver.py:209-213 analogue); buckets resume quicksort with a fresh budget
     rng = np.random.default_rng(5)
-    for n in (5000, 300000, 1 << 22):
+    for n in (20000, 300000, 1 << 22):  # above every base-case size (16384 for 4-byte keys)
         if dtype == "kv":
             keys = rng.integers(0, 50, n).astype(np.int64)
             vals = rng.integers(0, 2**32, n, dtype=np.uint32)
@@ -195,6 +195,32 @@ def test_forced_fallback_budget_zero(dtype):
         exp_k, exp_v = workloads.expected(keys, vals)
         assert same_bytes(got_k, exp_k) and (vals is None or same_bytes(got_v, exp_v)), n
         assert stats["radix_fallbacks"] >= 1
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.float32], ids=["int32", "float32"])
+def test_big_leaf_slow_paths(dtype):
+    # 4-byte keys-only leaves (<= 16384 keys) take k_base_big's slow paths when a bucket holds more than
+    # 32 keys: (a) clustered distinct keys with far outliers -> LSD radix passes over the whole leaf;
+    # (b) a large run of one repeated key beside distinct keys -> the constant bucket keeps its slots;
+    # (c) both at once inside a larger sort, so the leaves come out of partitions (data in A and in B)
+    rng = np.random.default_rng(11)
+    big = np.iinfo(np.int32) if dtype == np.int32 else None
+    lo, hi = (big.min, big.max) if big else (-np.inf, np.inf)
+    for n in (100, 5000, 12000, 16384):
+        k = rng.integers(0, 1000, n).astype(dtype)
+        k[rng.choice(n, 6, replace=False)] = [lo, hi, lo, hi, 0, 1]
+        got, _, _ = gpu_sort(k)
+        assert same_bytes(got, np.sort(k)), ("clustered", n)
+        k = np.concatenate([np.full(n // 2, 7), rng.integers(2**30, 2**31 - 1, n - n // 2)]).astype(dtype)
+        rng.shuffle(k)
+        got, _, _ = gpu_sort(k)
+        assert same_bytes(got, np.sort(k)), ("constant bucket", n)
+    n = 1 << 21
+    k = rng.integers(0, 5000, n).astype(dtype)
+    k[rng.choice(n, 64, replace=False)] = rng.integers(-2**31, 2**31 - 1, 64).astype(dtype)
+    k[rng.choice(n, n // 4, replace=False)] = dtype(12345)
+    got, _, stats = gpu_sort(k)
+    assert same_bytes(got, np.sort(k)) and stats["base_cases"] >= 1
 
 
 def test_bad_shift_one_exhausts_budgets_deep_in_the_tree():
