@@ -176,6 +176,12 @@ int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEven
     cudaError_t e = prepare<U, FLOAT, KV>(li);
     if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "setup: %s", cudaGetErrorString(e));
     const int sm = smem_bytes<U, FLOAT, KV>();
+    {  // tiles per task: the largest power of two <= 32 giving the root ~2 tasks per CTA
+        const int64_t per = ((P.n + TILE - 1) / TILE) / (2 * (int64_t)li.sms * li.occ);
+        uint32_t c = 1;
+        while (c < 32 && (int64_t)(c * 2) <= per) c *= 2;
+        P.chunk = c;
+    }
     if (P.use_check && P.n > 1) {
         const int64_t ch = (int64_t)THREADS * ITEMS;
         int64_t blocks = (P.n + ch - 1) / ch;

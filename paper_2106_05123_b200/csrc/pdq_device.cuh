@@ -112,6 +112,7 @@ struct Params {
     int debug_depth;   // > 0: segments at this depth are dropped unsorted (profiling only)
     uint64_t *leaves;  // queued leaves: begin << 16 | (size - 1) << 1 | in-B
     unsigned long long leaf_cap;
+    uint32_t chunk;    // tiles per ring task
 };
 
 // ---- key traits ----------------------------------------------------------------------

@@ -24,7 +24,14 @@
 
 namespace pdq {
 
-constexpr int CHUNK = 8;                // tiles per ring task (one claim + one descriptor read + one retire)
+// A ring task is a chunk of P.chunk consecutive tiles of one segment (one claim, one descriptor read,
+// one retire).  The host picks the chunk from the sort size: the largest power of two <= 32 that still
+// gives the top level ~2 tasks per CTA (32 tiles for 2^28 keys, 8 for 2^26).  A task word carries its
+// first tile.
+__device__ __forceinline__ uint32_t seg_ntasks(uint32_t N, uint32_t chunk) { return (N + chunk - 1) / chunk; }
+__device__ __forceinline__ uint32_t task_end_tile(uint32_t first, uint32_t N, uint32_t chunk) {
+    return min(first + chunk, N);
+}
 #ifndef PDQ_NST
 #define PDQ_NST 1
 #endif
@@ -66,7 +73,7 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, unsigned phase) {
 }
 
 struct Shared {
-    uint64_t bar[NST];       // TMA stage barriers
+    uint64_t bar[4];         // TMA stage barriers (Bufs::NSTAGE used)
     uint64_t task;           // current ring task word (0 = exit)
     Seg seg;                 // its descriptor
     uint64_t ntask;          // prefetched next task (0 = none / not yet published)
@@ -109,26 +116,33 @@ __device__ __forceinline__ uint32_t mix32(uint64_t x) {
     return (uint32_t)x;
 }
 
-// Dynamic shared memory of the persistent sorter: NST TMA stages and the compaction buffer kc
+// Dynamic shared memory of the persistent sorter: NSTAGE TMA stages and the compaction buffer kc
 // (keys, then payloads for KV).  Every pointer is computed arithmetically from the extern shared
-// symbol so the compiler emits LDS/STS, never generic LD/ST.
-// kc holds a tile's left and right runs, each placed at the 16-byte phase of its global destination
-// (so the run bodies leave by TMA bulk stores): up to KC_PAD elements of slack.
+// symbol so the compiler emits LDS/STS, never generic LD/ST.  kc holds a tile's left and right runs,
+// each placed at the 16-byte phase of its global destination (so the run bodies leave by TMA bulk
+// stores): KC_PAD elements of slack.  4-byte keys without payload use two stages (4 CTAs/SM), wider
+// elements one (their occupancy is bounded by shared memory already).
+// (Measured on 2^28 int32 and not kept: three stages with the tile compacted in place in its own
+// stage, and a software pipeline issuing tile t+1's reservation before tile t is compacted.)
 constexpr int KC_PAD = 16;
 template <class U, bool KV>
 struct Bufs {
-    static constexpr int KEY_BYTES = ((NST + 1) * TILE + KC_PAD) * (int)sizeof(U);
-    static constexpr int VAL_BYTES = KV ? ((NST + 1) * TILE + KC_PAD) * 4 : 0;
-    __device__ __forceinline__ static U *stage(int i) { return reinterpret_cast<U *>(g_dsm) + i * TILE; }
-    __device__ __forceinline__ static U *kc() { return reinterpret_cast<U *>(g_dsm) + NST * TILE; }
+    static constexpr int NSTAGE = (sizeof(U) == 4 && !KV) ? 2 : NST;
+    static constexpr int SLOT = TILE + KC_PAD;
+    static constexpr int KEY_BYTES = (NSTAGE + 1) * SLOT * (int)sizeof(U);
+    static constexpr int VAL_BYTES = KV ? (NSTAGE + 1) * SLOT * 4 : 0;
+    __device__ __forceinline__ static U *stage(int i) { return reinterpret_cast<U *>(g_dsm) + i * SLOT; }
+    __device__ __forceinline__ static U *kc() { return reinterpret_cast<U *>(g_dsm) + NSTAGE * SLOT; }
     __device__ __forceinline__ static uint32_t *vstage(int i) {
-        return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES) + i * TILE;
+        return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES) + i * SLOT;
     }
-    __device__ __forceinline__ static uint32_t *vc() { return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES) + NST * TILE; }
+    __device__ __forceinline__ static uint32_t *vc() {
+        return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES) + NSTAGE * SLOT;
+    }
     // pivot samples alias kc (free whenever samples are taken)
     __device__ __forceinline__ static uint64_t *samp_k() { return reinterpret_cast<uint64_t *>(kc()); }
     __device__ __forceinline__ static uint32_t *samp_v() {
-        return reinterpret_cast<uint32_t *>(reinterpret_cast<unsigned char *>(kc()) + SAMPLES * 8);
+        return reinterpret_cast<uint32_t *>(reinterpret_cast<unsigned char *>(samp_k()) + SAMPLES * 8);
     }
     __host__ __device__ static constexpr int bytes() { return KEY_BYTES + VAL_BYTES; }
 };
@@ -736,12 +750,15 @@ struct Sorter {
         }
     }
 
+    // T_PART: the segment's guided tasks (word = first tile); T_FILL: one task per tile
     __device__ static void push_tasks(const Params &P, uint32_t type, uint32_t sid, uint32_t ntiles) {
         Shared &sh = g_sh;
         const unsigned long long pos = sh.push_pos;
         const uint64_t mask = (1ull << P.log_q) - 1;
-        for (uint32_t t = threadIdx.x; t < ntiles; t += THREADS)
-            *(volatile uint64_t *)&P.ring[(pos + t) & mask] = task_word(pos + t, P.log_q, type, sid, t);
+        const uint32_t nt = type == T_PART ? seg_ntasks(ntiles, P.chunk) : ntiles;
+        for (uint32_t t = threadIdx.x; t < nt; t += THREADS)
+            *(volatile uint64_t *)&P.ring[(pos + t) & mask] =
+                task_word(pos + t, P.log_q, type, sid, type == T_PART ? t * P.chunk : t);
     }
 
     // ---- write [b, e) of A with the pivot (equal-key runs are bitwise identical under the
@@ -836,11 +853,11 @@ struct Sorter {
                 s->cnt_eq = 0;
                 s->tiles_done = 0;
                 __threadfence();
-                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)((ntiles + CHUNK - 1) / CHUNK));
+                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)seg_ntasks(ntiles, P.chunk));
             }
         }
         csync();
-        if (sh.new_sid < P.seg_cap) push_tasks(P, T_PART, sh.new_sid, (ntiles + CHUNK - 1) / CHUNK);
+        if (sh.new_sid < P.seg_cap) push_tasks(P, T_PART, sh.new_sid, ntiles);
         csync();
         if (depth > sh.s_max_depth && tid == 0) sh.s_max_depth = depth;
         return reuse_sid >= 0;
@@ -994,11 +1011,11 @@ struct Sorter {
                 s->cnt_eq = 0;
                 s->tiles_done = 0;
                 __threadfence();
-                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)((ntiles + CHUNK - 1) / CHUNK));
+                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)seg_ntasks(ntiles, P.chunk));
             }
         }
         csync();
-        if (sh.new_sid < P.seg_cap) push_tasks(P, T_PART, sh.new_sid, (ntiles + CHUNK - 1) / CHUNK);
+        if (sh.new_sid < P.seg_cap) push_tasks(P, T_PART, sh.new_sid, ntiles);
         csync();
         if (tid == 0) sh.s_cyc_spawn += clock64() - c0;
         return reuse_sid >= 0;
@@ -1093,7 +1110,7 @@ struct Sorter {
     // ---- thread 0: issue the TMA bulk load of tile `tile` of segment `sg` into the next stage ----------
     __device__ static void issue_load(const Params &P, const Seg &sg, uint32_t tile) {
         Shared &sh = g_sh;
-        const int st = (int)(sh.li % NST);
+        const int st = (int)(sh.li % B::NSTAGE);
         ++sh.li;
         const int64_t b = sg.begin, e = sg.end;
         const bool srcB = sg.info & I_SRC_B;
@@ -1138,8 +1155,6 @@ struct Sorter {
         }
     }
 
-    // Per-thread classification of ITEMS keys held in registers.  Thread t owns the VEC-key
-    // vectors q = jj*THREADS + t; lmask/vmask record left/valid per item.
     // Per-thread classification of the ITEMS keys of thread t (the VEC-key vectors
     // q = jj*THREADS + t); lmask/vmask record left/valid per item.
     template <bool FULL>
@@ -1171,7 +1186,7 @@ struct Sorter {
     // [ri, ...).  Ranks come from one ballot per item slot, so the 32 lanes of every store land in
     // two contiguous runs of kc (at most a 2-way bank conflict; a per-thread prefix would put
     // lanes ~8 words apart, an 8-way conflict).  Order within a side is free (no stability,
-    // PAPER.md:28-29).
+    // PAPER.md:28-29).  The keys are re-read from the stage (registers are the occupancy limit).
     template <bool FULL>
     __device__ __forceinline__ static void scatter(const U *sk, const uint32_t *sv, U *kc, uint32_t *vc,
                                                    unsigned lmask, unsigned vmask, int li, int ri) {
@@ -1202,11 +1217,10 @@ struct Sorter {
 
     // Store the run kc[a, a + len) (and vc) to dk[g, g + len) (and dv), a = g mod AL: the 16-byte
     // aligned body by one TMA bulk store per array (issued by thread 0, committed by the caller),
-    // the < AL-element head and tail by threads t0 + i.
-    __device__ __forceinline__ static void emit_run(U *dk, uint32_t *dv, long long g, int a, int len, int t0) {
+    // the < AL-element head and tail by threads t0 + i (warp 0).
+    __device__ __forceinline__ static void emit_run(const U *kc, const uint32_t *vc, U *dk, uint32_t *dv,
+                                                    long long g, int a, int len, int t0) {
         const int tid = threadIdx.x;
-        const U *kc = B::kc();
-        const uint32_t *vc = KV ? B::vc() : nullptr;
         int h = (int)((AL - (g & (AL - 1))) & (AL - 1));
         if (h > len) h = len;
         const int nb = ((len - h) / AL) * AL;
@@ -1258,14 +1272,14 @@ struct Sorter {
         const int64_t tbase = (b / TILE + tile) * (int64_t)TILE;
         const int64_t lo = b > tbase ? b : tbase;
         const int64_t hi = e < tbase + TILE ? e : tbase + TILE;
-        const int st = (int)(ci % NST);
+        const int st = (int)(ci % B::NSTAGE);
         const U *sk = B::stage(st);
         const uint32_t *sv = KV ? B::vstage(st) : nullptr;
         const U piv = (U)sg.pivot;
         const uint32_t pv = sg.pivot_v;
         const int lo_i = (int)(lo - tbase), hi_i = (int)(hi - tbase);
         const long long q0 = clock64();
-        mbar_wait(&sh.bar[st], (ci / NST) & 1u);
+        mbar_wait(&sh.bar[st], (ci / B::NSTAGE) & 1u);
         ++ci;
         const long long q1 = clock64();
         if (tid == 0) sh.s_sch_claim += q1 - q0;  // (profiling) stage wait
@@ -1343,8 +1357,8 @@ struct Sorter {
             sh.ci = ci;
             pump_loads(P);
         }
-        if (L && write_left) emit_run(dst, dstv, gl, aL, L, 0);
-        if (R) emit_run(dst, dstv, gr, aR, R, 64);
+        if (L && write_left) emit_run(kc, vc, dst, dstv, gl, aL, L, 1);
+        if (R) emit_run(kc, vc, dst, dstv, gr, aR, R, 8);
         if (tid == 0) bulk_commit();
         if (tid == 0) sh.s_sch_idle += clock64() - q1;  // (profiling) whole tile after the stage wait
     }
@@ -1353,10 +1367,10 @@ struct Sorter {
     // chunk and then, once it is published, the next task's chunk.
     __device__ __forceinline__ static void pump_loads(const Params &P) {
         Shared &sh = g_sh;
-        while (sh.li < sh.ci + NST) {
+        while (sh.li < sh.ci + B::NSTAGE) {
             if (sh.lslot == 0) {
                 if (sh.task && tile_task((uint32_t)(sh.task >> 45) & 7u)) {
-                    const uint32_t end = min(((uint32_t)(sh.task & 0x7FFFFF) + 1) * CHUNK, sh.seg.ntiles);
+                    const uint32_t end = task_end_tile((uint32_t)(sh.task & 0x7FFFFF), sh.seg.ntiles, P.chunk);
                     if (sh.ltile < end) {
                         issue_load(P, sh.seg, sh.ltile++);
                         continue;
@@ -1366,11 +1380,11 @@ struct Sorter {
                 if (sh.nstate == 1) poll_next(P);
                 if (sh.nstate != 2) return;
                 sh.lslot = 1;
-                sh.ltile = tile_task((uint32_t)(sh.ntask >> 45) & 7u) ? ((uint32_t)sh.ntask & 0x7FFFFF) * CHUNK : 0u;
+                sh.ltile = tile_task((uint32_t)(sh.ntask >> 45) & 7u) ? ((uint32_t)sh.ntask & 0x7FFFFF) : 0u;
             }
             // load cursor in the next task
             if (!tile_task((uint32_t)(sh.ntask >> 45) & 7u)) return;
-            const uint32_t end = min(((uint32_t)(sh.ntask & 0x7FFFFF) + 1) * CHUNK, sh.nseg.ntiles);
+            const uint32_t end = task_end_tile((uint32_t)(sh.ntask & 0x7FFFFF), sh.nseg.ntiles, P.chunk);
             if (sh.ltile >= end) return;
             issue_load(P, sh.nseg, sh.ltile++);
         }
@@ -1425,7 +1439,7 @@ struct Sorter {
         sh.task = sh.ntask;
         sh.seg = sh.nseg;
         sh.lslot = 0;
-        if (!cursor_ahead) sh.ltile = tile_task((uint32_t)(sh.task >> 45) & 7u) ? ((uint32_t)sh.task & 0x7FFFFF) * CHUNK : 0u;
+        if (!cursor_ahead) sh.ltile = tile_task((uint32_t)(sh.task >> 45) & 7u) ? ((uint32_t)sh.task & 0x7FFFFF) : 0u;
         // claim the following position now: its atomic overlaps the whole current task
         sh.npos = atomicAdd(&P.st->q_head, 1ull);
         sh.nstate = 1;
@@ -1976,8 +1990,9 @@ __global__ void __launch_bounds__(THREADS, base_min_blocks<U, KV>()) k_base(cons
 #endif
 template <class U, bool KV>
 constexpr int sort_min_blocks() {
-    if (PDQ_MINB > 0 && Bufs<U, KV>::bytes() <= 32 * 1024) return PDQ_MINB;
-    return Bufs<U, KV>::bytes() <= 37 * 1024 ? 6 : (Bufs<U, KV>::bytes() <= 50 * 1024 ? 4 : (Bufs<U, KV>::bytes() <= 74 * 1024 ? 3 : (Bufs<U, KV>::bytes() <= 108 * 1024 ? 2 : 1)));
+    // CTAs that fit in shared memory (+ static shared memory and the per-CTA reserve), capped
+    constexpr int fit = (228 * 1024) / (Bufs<U, KV>::bytes() + 2304);
+    return fit > PDQ_MINB ? PDQ_MINB : (fit < 1 ? 1 : fit);
 }
 
 template <class U, bool FLOAT, bool KV>
@@ -2005,7 +2020,7 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
     }
     if (tid == 0) {
         S::zero_counters();
-        for (int i = 0; i < NST; ++i) mbar_init(&sh.bar[i], 1);
+        for (int i = 0; i < S::B::NSTAGE; ++i) mbar_init(&sh.bar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         sh.li = sh.ci = 0;
         sh.lslot = 0;
@@ -2024,8 +2039,8 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
         const uint32_t type = (uint32_t)(w >> 45) & 7u;
         const uint32_t sid = (uint32_t)(w >> 23) & 0x3FFFFF;
         if (type == T_PART) {
-            const uint32_t t0 = ((uint32_t)w & 0x7FFFFF) * CHUNK;
-            const uint32_t t1 = min(t0 + CHUNK, sh.seg.ntiles);
+            const uint32_t t0 = (uint32_t)w & 0x7FFFFF;
+            const uint32_t t1 = task_end_tile(t0, sh.seg.ntiles, P.chunk);
             for (uint32_t t = t0; t < t1; ++t) S::part_tile(P, sid, t, ci);
             // retire the chunk: the bulk stores complete, one gpu-scope fence per thread, one
             // counter update per CTA
