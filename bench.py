@@ -258,10 +258,12 @@ def run_ours(args, rank, world, local_rank):
     clocks.__enter__()
     clocks.wait_first()
     # warmup (untimed)
+    stats = None
     for i in range(W):
         restore(i)
         ds.run(inputs[i % n_inputs])
-    stats = ds.finish()
+    if W:
+        stats = ds.finish()
     for i in range(W, W + K):
         restore(i)
     barrier()
