@@ -34,7 +34,7 @@ extern "C" void pdq_config_default(pdq_config *c) {
     c->use_partition_left = 1;
     c->use_break_patterns = 1;
     c->use_partial_insertion = 1;
-    c->base_case_size = BIG_BASE;
+    c->base_case_size = 16384;
     c->bad_budget = -1;
 }
 
@@ -49,7 +49,7 @@ extern "C" int pdq_config_validate(const pdq_config *c) {
     if (c->block_size < 1) return set_err(PDQ_ERR_CONFIG, "block_size must be >= 1%s");
     if (c->bad_partition_shift < 1) return set_err(PDQ_ERR_CONFIG, "bad_partition_shift must be >= 1%s");
     if (c->bad_partition_shift > 62) return set_err(PDQ_ERR_CONFIG, "bad_partition_shift must be <= 62%s");
-    if (c->base_case_size < 1024 || c->base_case_size > BIG_BASE)
+    if (c->base_case_size < 1024 || c->base_case_size > 16384)  // clamped per element type at launch
         return set_err(PDQ_ERR_CONFIG, "base_case_size must be in [1024, 16384]%s");
     return PDQ_OK;
 }
@@ -146,7 +146,9 @@ cudaError_t prepare(LaunchInfo &li) {
             if ((e = cudaFuncSetAttribute(k_base_big<FLOAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           BigLeaf<FLOAT>::bytes())) != cudaSuccess)
                 return e;
-            cached.occ_base = 1;
+            if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached.occ_base, k_base_big<FLOAT>, BigLeaf<FLOAT>::BT,
+                                                                   BigLeaf<FLOAT>::bytes())) != cudaSuccess)
+                return e;
         } else {
             const int smb = BaseBufs<U, KV>::bytes();
             if ((e = cudaFuncSetAttribute(k_base<U, FLOAT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb)) !=
@@ -194,7 +196,7 @@ int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEven
     k_sort<U, FLOAT, KV><<<(unsigned)(li.sms * li.occ), THREADS, sm, s>>>(P);
     if (ev1) cudaEventRecord(ev1, s);
     if constexpr (big_leaves<U, KV>())
-        k_base_big<FLOAT><<<(unsigned)li.sms, BigLeaf<FLOAT>::BT, BigLeaf<FLOAT>::bytes(), s>>>(P);
+        k_base_big<FLOAT><<<(unsigned)(li.sms * li.occ_base), BigLeaf<FLOAT>::BT, BigLeaf<FLOAT>::bytes(), s>>>(P);
     else
         k_base<U, FLOAT, KV><<<(unsigned)(li.sms * li.occ_base), THREADS, BaseBufs<U, KV>::bytes(), s>>>(P);
     e = cudaGetLastError();

@@ -1182,6 +1182,17 @@ struct Sorter {
         if (FULL) vmask = (1u << ITEMS) - 1;
     }
 
+    // ballot of (m & bit) != 0 (bit a compile-time constant after unrolling): one LOP3 to a predicate
+    // and one VOTE; the generic form costs a shift, a LOP3 and an ISETP more per item
+    __device__ __forceinline__ static unsigned ballot_bit(unsigned m, unsigned bit) {
+        unsigned b;
+        asm("{\n .reg .pred p;\n .reg .b32 t;\n and.b32 t, %1, %2;\n setp.ne.b32 p, t, 0;\n"
+            " vote.sync.ballot.b32 %0, p, 0xffffffff;\n}\n"
+            : "=r"(b)
+            : "r"(m), "r"(bit));
+        return b;
+    }
+
     // Branch-free compaction of this warp's keys into kc: its lefts fill [li, ...), its rights
     // [ri, ...).  Ranks come from one ballot per item slot, so the 32 lanes of every store land in
     // two contiguous runs of kc (at most a 2-way bank conflict; a per-thread prefix would put
@@ -1192,25 +1203,46 @@ struct Sorter {
                                                    unsigned lmask, unsigned vmask, int li, int ri) {
         const int tid = threadIdx.x;
         const unsigned ltm = lanemask_lt();
+        if constexpr (FULL) {
+            // every lane holds a valid item in every round: a right's rank is (lane - lefts before it),
+            // so one ballot and two popcounts per round place all 32 items
+            int rw = ri + (tid & 31);
 #pragma unroll
-        for (int jj = 0; jj < ITEMS / VEC; ++jj) {
-            const int q = jj * THREADS + tid;
-            U kk[VEC];
-            ldvec(sk, q, kk);
+            for (int jj = 0; jj < ITEMS / VEC; ++jj) {
+                const int q = jj * THREADS + tid;
+                U kk[VEC];
+                ldvec(sk, q, kk);
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-                const int r = jj * VEC + e;
-                const bool isl = (lmask >> r) & 1u;
-                const bool valid = FULL || ((vmask >> r) & 1u);
-                const unsigned bl = __ballot_sync(0xffffffffu, isl);
-                const unsigned br = FULL ? ~bl : __ballot_sync(0xffffffffu, valid && !isl);
-                const int pos = isl ? li + __popc(bl & ltm) : ri + __popc(br & ltm);
-                if (valid) {
+                for (int e = 0; e < VEC; ++e) {
+                    const unsigned bl = ballot_bit(lmask, 1u << (jj * VEC + e));
+                    const bool isl = (bl >> (tid & 31)) & 1u;
+                    const int d = __popc(bl & ltm), c = __popc(bl);
+                    const int pos = isl ? li + d : rw - d;
                     kc[pos] = kk[e];
                     if (KV) vc[pos] = sv[q * VEC + e];
+                    li += c;
+                    rw += 32 - c;
                 }
-                li += __popc(bl);
-                ri += __popc(br);
+            }
+        } else {
+#pragma unroll
+            for (int jj = 0; jj < ITEMS / VEC; ++jj) {
+                const int q = jj * THREADS + tid;
+                U kk[VEC];
+                ldvec(sk, q, kk);
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) {
+                    const unsigned bit = 1u << (jj * VEC + e);
+                    const unsigned bl = ballot_bit(lmask, bit), br = ballot_bit(vmask, bit) & ~bl;
+                    const unsigned me = 1u << (tid & 31);
+                    const int pos = (bl & me) ? li + __popc(bl & ltm) : ri + __popc(br & ltm);
+                    if ((bl | br) & me) {
+                        kc[pos] = kk[e];
+                        if (KV) vc[pos] = sv[q * VEC + e];
+                    }
+                    li += __popc(bl);
+                    ri += __popc(br);
+                }
             }
         }
     }
