@@ -1772,14 +1772,14 @@ struct BigLeaf {
 
     // Slow path (a bucket holds more than CMAX keys).  kc holds the bucketed leaf and cnt the
     // (start, count) words; writes kd[a0 + i] = raw keys in order.
-    __device__ __noinline__ static void slow_leaf(int m, int a0, const Map mp, U range, const uint32_t (&pp)[BI / 2]) {
+    __device__ __noinline__ static void slow_leaf(int m, int a0, const Map mp, U range) {
         const int tid = threadIdx.x;
         uint32_t *kc = wd(), *kd = wd() + KD_OFF, *cnt = wd() + CNT_OFF;
         int fb = 0;
 #pragma unroll
         for (int j = 0; j < BI; ++j) {
             if (j * BT + tid < m) {
-                const uint32_t p = (pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu;
+                const uint32_t p = j * BT + tid;
                 const U x = kc[p];
                 const uint32_t sc = cnt[mp(x)];
                 if ((sc >> 16) > (uint32_t)CMAX && kc[sc & 0xFFFFu] != x) fb = 1;  // a big mixed bucket
@@ -1790,7 +1790,7 @@ struct BigLeaf {
 #pragma unroll
             for (int j = 0; j < BI; ++j) {
                 if (j * BT + tid < m) {
-                    const uint32_t p = (pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu;
+                    const uint32_t p = j * BT + tid;
                     const U x = kc[p];
                     const uint32_t sc = cnt[mp(x)];
                     const uint32_t r = (sc >> 16) > (uint32_t)CMAX ? p : rank_in_bucket(kc, x, p, sc);
@@ -1889,7 +1889,7 @@ struct BigLeaf {
                 continue;
             }
             const Map mp = make_map(mn, range);
-            uint32_t pp[BI / 2];  // 16-bit slots, then 16-bit positions in kc
+            uint32_t pp[BI / 2];  // 16-bit slots
 #pragma unroll
             for (int j = 0; j < BI; ++j) {
                 const uint32_t sl = (j * BT + tid < m) ? atomicAdd(&cnt[mp(xs[j])], 1u) : 0u;
@@ -1927,10 +1927,7 @@ struct BigLeaf {
 #pragma unroll
             for (int j = 0; j < BI; ++j) {
                 if (j * BT + tid < m) {
-                    const uint32_t sh16 = (j & 1) << 4;
-                    const uint32_t p = (cnt[mp(xs[j])] & 0xFFFFu) + ((pp[j / 2] >> sh16) & 0xFFFFu);
-                    kc[p] = xs[j];
-                    pp[j / 2] = (pp[j / 2] & ~(0xFFFFu << sh16)) | (p << sh16);
+                    kc[(cnt[mp(xs[j])] & 0xFFFFu) + ((pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu)] = xs[j];
                 }
             }
             const int a0 = (int)(b & 3);
@@ -1939,15 +1936,15 @@ struct BigLeaf {
             if (cmax <= (uint32_t)CMAX) {
                 load(P, nxt, xs);  // the next leaf's loads fly while this one is ranked and stored
 #pragma unroll
-                for (int j = 0; j < BI; ++j) {
+                for (int j = 0; j < BI; ++j) {  // kc in position order: no per-key state carried over
                     if (j * BT + tid < m) {
-                        const uint32_t p = (pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu;
+                        const uint32_t p = j * BT + tid;
                         const U x = kc[p];
                         kd[a0 + rank_in_bucket(kc, x, p, cnt[mp(x)])] = O::from(x);
                     }
                 }
             } else {
-                slow_leaf(m, a0, mp, range, pp);
+                slow_leaf(m, a0, mp, range);
                 load(P, nxt, xs);
             }
             fence_proxy_async();
