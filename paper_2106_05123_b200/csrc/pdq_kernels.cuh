@@ -1839,7 +1839,13 @@ struct BigLeaf {
         load(P, cur, xs);
         while (cur != NONE) {
             const long long c0 = clock64();
-            claim(k ^ 1);
+            // thread 0 claims the next leaf; its descriptor stays in a register until the barrier before
+            // the ranking phase, so the round trips never stall the barriers in between
+            uint64_t pend = NONE;
+            if (tid == 0) {
+                const unsigned long long idx = atomicAdd(&P.st->leaf_next, 1ull);
+                if (idx < count) pend = ldcg(P.leaves + idx);
+            }
             const int m = (int)((cur >> 1) & 0x7FFF) + 1;
             const int64_t b = (int64_t)(cur >> 16);
             const bool srcB = cur & 1u;
@@ -1867,7 +1873,6 @@ struct BigLeaf {
             bsync();
             mn = __reduce_min_sync(0xffffffffu, red[64 + lane]);
             mx = __reduce_max_sync(0xffffffffu, red[96 + lane]);
-            const uint64_t nxt = sh.lf[k ^ 1];  // written by thread 0 before the barrier above
             const U range = mx - mn;
             if (range == 0) {
                 // a constant leaf is sorted; one in B is copied to its place in A
@@ -1877,14 +1882,15 @@ struct BigLeaf {
                     for (int j = 0; j < BI; ++j)
                         if (j * BT + tid < m) a[j * BT + tid] = O::from(xs[j]);
                 }
-                load(P, nxt, xs);
                 if (tid == 0) {
+                    sh.lf[k ^ 1] = pend;
                     sh.s_base++;
                     sh.s_bytes += (srcB ? 2ull : 1ull) * 4 * m;
                     sh.s_cyc_base += clock64() - c0;
                 }
                 bsync();
-                cur = nxt;
+                cur = sh.lf[k ^ 1];
+                load(P, cur, xs);
                 k ^= 1;
                 continue;
             }
@@ -1931,8 +1937,12 @@ struct BigLeaf {
                 }
             }
             const int a0 = (int)(b & 3);
-            if (tid == 0) bulk_wait_read();  // the previous leaf's bulk store has left kd
+            if (tid == 0) {
+                bulk_wait_read();  // the previous leaf's bulk store has left kd
+                sh.lf[k ^ 1] = pend;
+            }
             bsync();
+            const uint64_t nxt = sh.lf[k ^ 1];
             if (cmax <= (uint32_t)CMAX) {
                 load(P, nxt, xs);  // the next leaf's loads fly while this one is ranked and stored
 #pragma unroll
