@@ -11,6 +11,7 @@ from .driver import (
     DEFAULT_CONFIG,
     MIN_BREAK_SIZE,
     DeviceSorter,
+    HostPipeline,
     SortConfig,
     is_bad_partition,
     sort,
@@ -24,6 +25,7 @@ __version__ = "0.1.0"
 __all__ = [
     "DEFAULT_CONFIG",
     "DeviceSorter",
+    "HostPipeline",
     "MIN_BREAK_SIZE",
     "SortConfig",
     "is_bad_partition",

@@ -214,6 +214,65 @@ def sort_device(keys, values=None, config: SortConfig = DEFAULT_CONFIG) -> dict:
     return stats
 
 
+class HostPipeline:
+    """Sort a stream of host batches: H2D of batch i+1, the sort of batch i and the D2H of batch i-1
+    run concurrently on three streams (two copy engines + the SMs), with ``depth`` device buffers.
+
+    ``sort(inputs, outputs)``: ``inputs[i]`` / ``outputs[i]`` are 1-D CPU tensors of n keys (pinned
+    for asynchronous copies); ``outputs[i]`` receives batch i sorted.  Returns after every batch
+    has been copied back.  This is the serving-side use of the stream-ordered C ABI: each batch
+    is one ``pdq_sort`` call on the sort stream.
+    """
+
+    def __init__(self, n: int, dtype, device=None, config: SortConfig = DEFAULT_CONFIG, depth: int = 3):
+        import torch
+
+        self.device = torch.device(device or "cuda")
+        self.n, self.depth = int(n), int(depth)
+        self.sorter = DeviceSorter(n, dtype, False, self.device, config)
+        self.bufs = [torch.empty(self.n, dtype=dtype, device=self.device) for _ in range(self.depth)]
+        self.s_h2d = torch.cuda.Stream(self.device)
+        self.s_sort = torch.cuda.Stream(self.device)
+        self.s_d2h = torch.cuda.Stream(self.device)
+
+    def sort(self, inputs, outputs, events=None):
+        """``events=(begin, end)``: torch.cuda.Events (enable_timing) recorded before the first H2D and
+        after the last D2H."""
+        import torch
+
+        if len(inputs) != len(outputs):
+            raise ValueError("inputs and outputs must pair up")
+        ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
+        h2d_done, sort_done, d2h_done = [], [], []
+        if events is not None:
+            events[0].record(self.s_h2d)
+            self.s_sort.wait_event(events[0])
+            self.s_d2h.wait_event(events[0])
+        for i, (src, dst) in enumerate(zip(inputs, outputs)):
+            if src.numel() != self.n or dst.numel() != self.n:
+                raise TypeError("every batch must hold n keys")
+            buf = self.bufs[i % self.depth]
+            if i >= self.depth:
+                self.s_h2d.wait_event(d2h_done[i - self.depth])  # the buffer's previous batch is home
+            with torch.cuda.stream(self.s_h2d):
+                buf.copy_(src, non_blocking=True)
+            h2d_done.append(ev())
+            h2d_done[-1].record(self.s_h2d)
+            self.s_sort.wait_event(h2d_done[-1])
+            self.sorter.run(buf, stream=self.s_sort)
+            sort_done.append(ev())
+            sort_done[-1].record(self.s_sort)
+            self.s_d2h.wait_event(sort_done[-1])
+            with torch.cuda.stream(self.s_d2h):
+                dst.copy_(buf, non_blocking=True)
+            d2h_done.append(ev())
+            d2h_done[-1].record(self.s_d2h)
+        if events is not None:
+            events[1].record(self.s_d2h)
+        self.s_d2h.synchronize()
+        return self.sorter.finish(stream=self.s_sort)
+
+
 # ---------------------------------------------------------------------------------------------
 # host containers -> device -> back in place
 

@@ -345,3 +345,19 @@ def test_repeated_sorts_reuse_workspace():
         ds.run(d)
         ds.finish()
         assert np.array_equal(d.cpu().numpy(), np.sort(a))
+
+
+def test_host_pipeline_batches():
+    # HostPipeline (the serving-side host-batch path used by bench.py's e2e leg): every batch sorted,
+    # buffers recycled across more batches than device buffers
+    from paper_2106_05123_b200 import HostPipeline
+
+    rng = np.random.default_rng(21)
+    n = 300001
+    for dtype, tdt in ((np.int32, torch.int32), (np.float32, torch.float32)):
+        ins = [torch.from_numpy(shapes(n, rng, dtype)[name].copy()).pin_memory()
+               for name in ("uniform", "dups16", "desc", "organ", "asc_tail", "uniform", "dupsq")]
+        outs = [torch.empty_like(x).pin_memory() for x in ins]
+        HostPipeline(n, tdt, depth=3).sort(ins, outs)
+        for x, y in zip(ins, outs):
+            assert same_bytes(y.numpy(), oracle_sort(x.numpy())[0])
