@@ -10,6 +10,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include <type_traits>
 
@@ -198,6 +199,23 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     return t;
 }
 constexpr uint64_t WATCHDOG_NS = 10ull * 1000 * 1000 * 1000;
+
+// Debug builds (-DPDQ_DEBUG, tools/build_debug.sh): device-side bounds / invariant checks that trap
+// with a message (compute-sanitizer is not available on the GPU pool).  Compiled out otherwise.
+#ifdef PDQ_DEBUG
+#define PDQ_CHECK(cond, what)                                                                        \
+    do {                                                                                             \
+        if (!(cond)) {                                                                               \
+            printf("PDQ_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,    \
+                   (int)blockIdx.x, (int)threadIdx.x);                                               \
+            __trap();                                                                                \
+        }                                                                                            \
+    } while (0)
+#else
+#define PDQ_CHECK(cond, what) \
+    do {                      \
+    } while (0)
+#endif
 
 template <class U>
 __device__ __forceinline__ U ldcg(const U *p) {

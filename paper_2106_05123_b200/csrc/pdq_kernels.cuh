@@ -1035,6 +1035,7 @@ struct Sorter {
         }
         csync();
         const int64_t b = sg.begin, e = sg.end, m = e - b, L = sh.fL;
+        PDQ_CHECK(L >= 0 && L <= m, "finalized left count");
         const bool srcB = sg.info & I_SRC_B, dstB = !srcB;
         const uint64_t piv_ord = (uint64_t)O::to((U)sg.pivot);
         if (sg.info & I_RADIX) {
@@ -1218,6 +1219,7 @@ struct Sorter {
                     const bool isl = (bl >> (tid & 31)) & 1u;
                     const int d = __popc(bl & ltm), c = __popc(bl);
                     const int pos = isl ? li + d : rw - d;
+                    PDQ_CHECK(pos >= 0 && pos < B::SLOT, "partition compaction slot");
                     kc[pos] = kk[e];
                     if (KV) vc[pos] = sv[q * VEC + e];
                     li += c;
@@ -1237,6 +1239,7 @@ struct Sorter {
                     const unsigned me = 1u << (tid & 31);
                     const int pos = (bl & me) ? li + __popc(bl & ltm) : ri + __popc(br & ltm);
                     if ((bl | br) & me) {
+                        PDQ_CHECK(pos >= 0 && pos < B::SLOT, "partition compaction slot (edge tile)");
                         kc[pos] = kk[e];
                         if (KV) vc[pos] = sv[q * VEC + e];
                     }
@@ -1360,6 +1363,7 @@ struct Sorter {
                 if (E) atomicAdd(&gs->cnt_eq, (unsigned long long)E);
             }
             const long long gl = b + lOff, gr = e - rOff - R;
+            PDQ_CHECK(gl >= b && gl + L <= gr && gr + R <= e, "tile reservation inside its segment");
             const int aL = (int)(gl & (AL - 1));
             const int aR = aL + L + (int)((gr - (aL + L)) & (AL - 1));
             sh.lOff = gl;
@@ -1933,6 +1937,9 @@ struct BigLeaf {
 #pragma unroll
             for (int j = 0; j < BI; ++j) {
                 if (j * BT + tid < m) {
+                    PDQ_CHECK(mp(xs[j]) < (uint32_t)BBK, "leaf bucket");
+                    PDQ_CHECK((cnt[mp(xs[j])] & 0xFFFFu) + ((pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu) < (uint32_t)m,
+                              "leaf scatter slot");
                     kc[(cnt[mp(xs[j])] & 0xFFFFu) + ((pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu)] = xs[j];
                 }
             }
@@ -1950,7 +1957,9 @@ struct BigLeaf {
                     if (j * BT + tid < m) {
                         const uint32_t p = j * BT + tid;
                         const U x = kc[p];
-                        kd[a0 + rank_in_bucket(kc, x, p, cnt[mp(x)])] = O::from(x);
+                        const uint32_t r = rank_in_bucket(kc, x, p, cnt[mp(x)]);
+                        PDQ_CHECK(r < (uint32_t)m, "leaf rank");
+                        kd[a0 + r] = O::from(x);
                     }
                 }
             } else {
