@@ -94,7 +94,7 @@ Layout layout(int dtype, int has_payload, int64_t n) {
     L.segs = off;
     off += a256(segs * sizeof(Seg));
     // outstanding tasks <= tiles of live (disjoint) segments + claimed-but-unprocessed
-    uint64_t q = (uint64_t)n / TILE + 2 * ((uint64_t)n / MIN_BASE) + 2 * segs + 16384;
+    uint64_t q = (uint64_t)n / (TILE / 2) + 2 * ((uint64_t)n / MIN_BASE) + 2 * segs + 16384;  // tiles >= TILE/2
     int lq = 14;
     while ((1ull << lq) < q) ++lq;
     L.log_q = lq;
@@ -179,7 +179,8 @@ int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEven
     if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "setup: %s", cudaGetErrorString(e));
     const int sm = smem_bytes<U, FLOAT, KV>();
     {  // tiles per task: the largest power of two <= 32 giving the root ~2 tasks per CTA
-        const int64_t per = ((P.n + TILE - 1) / TILE) / (2 * (int64_t)li.sms * li.occ);
+        constexpr int TL = Sorter<U, FLOAT, KV>::TL;
+        const int64_t per = ((P.n + TL - 1) / TL) / (2 * (int64_t)li.sms * li.occ);
         uint32_t c = 1;
         while (c < 32 && (int64_t)(c * 2) <= per) c *= 2;
         P.chunk = c;
@@ -228,7 +229,7 @@ extern "C" int pdq_sort_ex(void *keys, int dtype, uint32_t *payload, int64_t n, 
     if (rc) return rc;
     if (dtype_size(dtype) == 0) return set_err(PDQ_ERR_DTYPE, "unsupported dtype code%s");
     if (n < 0) return set_err(PDQ_ERR_ARG, "n must be >= 0%s");
-    if (n > ((int64_t)MAX_TILES - 2) * TILE) return set_err(PDQ_ERR_ARG, "n too large for the task encoding%s");
+    if (n > ((int64_t)MAX_TILES - 2) * (TILE / 2)) return set_err(PDQ_ERR_ARG, "n too large for the task encoding%s");
     if (n > 0 && !keys) return set_err(PDQ_ERR_ARG, "keys is NULL%s");
     if (((uintptr_t)keys & 15) || ((uintptr_t)payload & 15))
         return set_err(PDQ_ERR_ALIGN, "keys and payload must be 16-byte aligned%s");

@@ -127,8 +127,9 @@ __device__ __forceinline__ uint32_t mix32(uint64_t x) {
 constexpr int KC_PAD = 16;
 template <class U, bool KV>
 struct Bufs {
-    static constexpr int NSTAGE = (sizeof(U) == 4 && !KV) ? 2 : NST;
-    static constexpr int SLOT = TILE + KC_PAD;
+    static constexpr int TLB = (sizeof(U) + (KV ? 4 : 0)) > 4 ? TILE / 2 : TILE;  // elements per tile
+    static constexpr int NSTAGE = 2;
+    static constexpr int SLOT = TLB + KC_PAD;
     static constexpr int KEY_BYTES = (NSTAGE + 1) * SLOT * (int)sizeof(U);
     static constexpr int VAL_BYTES = KV ? (NSTAGE + 1) * SLOT * 4 : 0;
     __device__ __forceinline__ static U *stage(int i) { return reinterpret_cast<U *>(g_dsm) + i * SLOT; }
@@ -174,6 +175,9 @@ struct Sorter {
     static constexpr int VEC = 16 / sizeof(U);
     static constexpr int AL = KV ? 4 : VEC;  // element alignment making both key and payload 16 B aligned
     static constexpr int ELEM_BYTES = sizeof(U) + (KV ? 4 : 0);
+    // partition tile: 4096 elements of 4 bytes, 2048 of wider elements (16-24 KB per TMA stage, so the
+    // persistent sorter keeps two stages and 3-4 CTAs per SM for every element type)
+    static constexpr int TL = B::TLB, IT = TL / THREADS;
     using SU = typename std::conditional<sizeof(U) == 4, int32_t, int64_t>::type;
     
     static constexpr int KBITS = 8 * (int)sizeof(U);
@@ -782,7 +786,7 @@ struct Sorter {
             csync();
             return false;
         }
-        const uint32_t ntiles = (uint32_t)((e - 1) / TILE - b / TILE + 1);
+        const uint32_t ntiles = (uint32_t)((e - 1) / TL - b / TL + 1);
         if (tid == 0) {
             uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
             sh.new_sid = sid;
@@ -829,7 +833,7 @@ struct Sorter {
             tk |= (uint64_t)((U)1 << (KBITS - 1 - bit));
         else
             tv |= 1u << (31 - (bit - KBITS));
-        const uint32_t ntiles = (uint32_t)((e - 1) / TILE - b / TILE + 1);
+        const uint32_t ntiles = (uint32_t)((e - 1) / TL - b / TL + 1);
         if (tid == 0) {
             const uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
             sh.new_sid = sid;
@@ -983,7 +987,7 @@ struct Sorter {
         const bool dup_heavy = lo_sample == piv;  // the low end of the sample repeats the pivot
         // driver.py:222: a predecessor not less than the pivot equals it -> partition_left
         const bool left = P.use_left && has_lb && !pless<KV>(lb, lbv, piv, pv);
-        const uint32_t ntiles = (uint32_t)((e - 1) / TILE - b / TILE + 1);
+        const uint32_t ntiles = (uint32_t)((e - 1) / TL - b / TL + 1);
         if (tid == 0) {
             uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
             sh.new_sid = sid;
@@ -1117,9 +1121,9 @@ struct Sorter {
         const bool srcB = sg.info & I_SRC_B;
         const U *src = (const U *)(srcB ? P.b_keys : P.a_keys);
         const uint32_t *srcv = srcB ? P.b_vals : P.a_vals;
-        const int64_t tbase = (b / TILE + tile) * (int64_t)TILE;
+        const int64_t tbase = (b / TL + tile) * (int64_t)TL;
         const int64_t lo = b > tbase ? b : tbase;
-        const int64_t hi = e < tbase + TILE ? e : tbase + TILE;
+        const int64_t hi = e < tbase + TL ? e : tbase + TL;
         const int64_t nfl = P.n & ~(int64_t)(AL - 1);
         const int64_t lo_al = lo & ~(int64_t)(AL - 1);
         int64_t hi_al = (hi + AL - 1) & ~(int64_t)(AL - 1);
@@ -1156,7 +1160,7 @@ struct Sorter {
         }
     }
 
-    // Per-thread classification of the ITEMS keys of thread t (the VEC-key vectors
+    // Per-thread classification of the IT keys of thread t (the VEC-key vectors
     // q = jj*THREADS + t); lmask/vmask record left/valid per item.
     template <bool FULL>
     __device__ __forceinline__ static void classify(const U *sk, const uint32_t *sv, int lo_i, int hi_i, U piv,
@@ -1164,7 +1168,7 @@ struct Sorter {
                                                     unsigned &vmask, int &eqc) {
         const int tid = threadIdx.x;
 #pragma unroll
-        for (int jj = 0; jj < ITEMS / VEC; ++jj) {
+        for (int jj = 0; jj < IT / VEC; ++jj) {
             const int q = jj * THREADS + tid;
             U kk[VEC];
             ldvec(sk, q, kk);
@@ -1180,7 +1184,7 @@ struct Sorter {
                 if (count_eq) eqc += (valid && kk[e] == piv && (!KV || v == pv)) ? 1 : 0;
             }
         }
-        if (FULL) vmask = (1u << ITEMS) - 1;
+        if (FULL) vmask = (1u << IT) - 1;
     }
 
     // ballot of (m & bit) != 0 (bit a compile-time constant after unrolling): one LOP3 to a predicate
@@ -1209,7 +1213,7 @@ struct Sorter {
             // so one ballot and two popcounts per round place all 32 items
             int rw = ri + (tid & 31);
 #pragma unroll
-            for (int jj = 0; jj < ITEMS / VEC; ++jj) {
+            for (int jj = 0; jj < IT / VEC; ++jj) {
                 const int q = jj * THREADS + tid;
                 U kk[VEC];
                 ldvec(sk, q, kk);
@@ -1228,7 +1232,7 @@ struct Sorter {
             }
         } else {
 #pragma unroll
-            for (int jj = 0; jj < ITEMS / VEC; ++jj) {
+            for (int jj = 0; jj < IT / VEC; ++jj) {
                 const int q = jj * THREADS + tid;
                 U kk[VEC];
                 ldvec(sk, q, kk);
@@ -1304,9 +1308,9 @@ struct Sorter {
         const bool left_mode = sg.info & I_LEFT;
         const bool count_eq = (sg.info & I_COUNT_EQ) && !left_mode;
         const bool packed = (e - b) < (1ll << 32);
-        const int64_t tbase = (b / TILE + tile) * (int64_t)TILE;
+        const int64_t tbase = (b / TL + tile) * (int64_t)TL;
         const int64_t lo = b > tbase ? b : tbase;
-        const int64_t hi = e < tbase + TILE ? e : tbase + TILE;
+        const int64_t hi = e < tbase + TL ? e : tbase + TL;
         const int st = (int)(ci % B::NSTAGE);
         const U *sk = B::stage(st);
         const uint32_t *sv = KV ? B::vstage(st) : nullptr;
@@ -1320,7 +1324,7 @@ struct Sorter {
         if (tid == 0) sh.s_sch_claim += q1 - q0;  // (profiling) stage wait
         unsigned lmask = 0, vmask = 0;
         int eqc = 0;
-        if (lo_i == 0 && hi_i == TILE)
+        if (lo_i == 0 && hi_i == TL)
             classify<true>(sk, sv, lo_i, hi_i, piv, pv, left_mode, count_eq, lmask, vmask, eqc);
         else
             classify<false>(sk, sv, lo_i, hi_i, piv, pv, left_mode, count_eq, lmask, vmask, eqc);
@@ -1380,7 +1384,7 @@ struct Sorter {
         const int li0 = aL + (int)(wpre & 0xFFFF), ri0 = aR + (int)(wpre >> 16);  // this warp's runs in kc
         U *kc = B::kc();
         uint32_t *vc = KV ? B::vc() : nullptr;
-        if (lo_i == 0 && hi_i == TILE)  // CTA-uniform (the ballots need every lane)
+        if (lo_i == 0 && hi_i == TL)  // CTA-uniform (the ballots need every lane)
             scatter<true>(sk, sv, kc, vc, lmask, vmask, li0, ri0);
         else
             scatter<false>(sk, sv, kc, vc, lmask, vmask, li0, ri0);
@@ -1484,9 +1488,9 @@ struct Sorter {
 
     __device__ static void fill_tile(const Params &P, const Seg &sg, uint32_t tile) {
         Shared &sh = g_sh;
-        const int64_t tbase = (sg.begin / TILE + tile) * (int64_t)TILE;
+        const int64_t tbase = (sg.begin / TL + tile) * (int64_t)TL;
         const int64_t lo = sg.begin > tbase ? sg.begin : tbase;
-        const int64_t hi = sg.end < tbase + TILE ? sg.end : tbase + TILE;
+        const int64_t hi = sg.end < tbase + TL ? sg.end : tbase + TL;
         const U raw = O::from((U)sg.pivot);
         const uint32_t pv = sg.pivot_v;
         store_run<U>((U *)P.a_keys + lo, (int)(hi - lo), [&](int) { return raw; });
