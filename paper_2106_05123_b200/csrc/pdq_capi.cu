@@ -173,7 +173,8 @@ cudaError_t prepare(LaunchInfo &li) {
 template <class U, bool FLOAT, bool KV>
 int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEvent_t ev1) {
     LaunchInfo li;
-    const int base_max = big_leaves<U, KV>() ? BIG_BASE : MAX_BASE;
+    // (k_base_big reads a leaf as 16-byte vectors from its aligned base: up to 3 slots of lead-in)
+    const int base_max = big_leaves<U, KV>() ? BIG_BASE - 4 : MAX_BASE;
     if (P.base_size > base_max) P.base_size = base_max;
     cudaError_t e = prepare<U, FLOAT, KV>(li);
     if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "setup: %s", cudaGetErrorString(e));

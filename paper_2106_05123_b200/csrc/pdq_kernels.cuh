@@ -1668,15 +1668,38 @@ struct BigLeaf {
         return (warp ? wpre : 0u) + inc - v;
     }
 
+    // Register j of thread t holds leaf element eidx(j) = 4 ((j / 4) BT + t) + j % 4 - (b mod 4): the
+    // leaf is read as 16-byte vectors from its 16-byte-aligned base (a quarter of the load
+    // instructions of a scalar layout); slots outside [0, m) are padding.
+    __device__ __forceinline__ static int eidx(int j, int off) {
+        return 4 * ((j >> 2) * BT + (int)threadIdx.x) + (j & 3) - off;
+    }
     __device__ __forceinline__ static void load(const Params &P, uint64_t lf, U (&xs)[BI]) {
         const int tid = threadIdx.x;
         const int m = lf == ~0ull ? 0 : (int)((lf >> 1) & 0x7FFF) + 1;
+        PDQ_CHECK(m <= BIG_BASE - 3, "leaf fits the vector layout (m + b mod 4 <= BIG_BASE)");
         const int64_t b = (int64_t)(lf >> 16);
-        const U *src = (const U *)((lf & 1u) ? P.b_keys : P.a_keys);
+        const int off = (int)(b & 3);
+        const U *src = (const U *)((lf & 1u) ? P.b_keys : P.a_keys) + (b - off);
+        const int64_t room = P.n - (b - off);  // elements readable from the aligned base
 #pragma unroll
-        for (int j = 0; j < BI; ++j) {
-            const int i = j * BT + tid;
-            xs[j] = i < m ? ldcg(src + b + i) : 0u;
+        for (int jv = 0; jv < BI / 4; ++jv) {
+            const int e0 = 4 * (jv * BT + tid);  // first slot of this vector (before the offset)
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (m > 0 && e0 < off + m && e0 + 4 > off) {  // the vector holds an element of the leaf
+                PDQ_CHECK((b - off) + e0 >= 0 && (b - off) + e0 < P.n, "leaf vector load in the array");
+                if (e0 + 4 <= room) {
+                    v = __ldcg(reinterpret_cast<const uint4 *>(src + e0));
+                } else {  // the array's last partial vector: scalar reads
+                    v.x = ldcg(src + e0);
+                    if (e0 + 1 < room) v.y = ldcg(src + e0 + 1);
+                    if (e0 + 2 < room) v.z = ldcg(src + e0 + 2);
+                }
+            }
+            xs[4 * jv] = v.x;
+            xs[4 * jv + 1] = v.y;
+            xs[4 * jv + 2] = v.z;
+            xs[4 * jv + 3] = v.w;
         }
     }
 
@@ -1862,10 +1885,11 @@ struct BigLeaf {
 #pragma unroll
                 for (int q = 0; q < BBK / 4 / BT; ++q) c4[q * BT + tid] = make_uint4(0, 0, 0, 0);
             }
+            const int off = (int)(b & 3);
             U mn = ~0u, mx = 0u;
 #pragma unroll
             for (int j = 0; j < BI; ++j) {
-                if (j * BT + tid < m) {
+                if ((unsigned)eidx(j, off) < (unsigned)m) {
                     const U x = O::to(xs[j]);
                     xs[j] = x;
                     mn = min(mn, x);
@@ -1888,7 +1912,7 @@ struct BigLeaf {
                     U *a = (U *)P.a_keys + b;
 #pragma unroll
                     for (int j = 0; j < BI; ++j)
-                        if (j * BT + tid < m) a[j * BT + tid] = O::from(xs[j]);
+                        if ((unsigned)eidx(j, off) < (unsigned)m) a[eidx(j, off)] = O::from(xs[j]);
                 }
                 if (tid == 0) {
                     sh.lf[k ^ 1] = pend;
@@ -1906,7 +1930,7 @@ struct BigLeaf {
             uint32_t pp[BI / 2];  // 16-bit slots
 #pragma unroll
             for (int j = 0; j < BI; ++j) {
-                const uint32_t sl = (j * BT + tid < m) ? atomicAdd(&cnt[mp(xs[j])], 1u) : 0u;
+                const uint32_t sl = ((unsigned)eidx(j, off) < (unsigned)m) ? atomicAdd(&cnt[mp(xs[j])], 1u) : 0u;
                 if (j & 1) pp[j / 2] |= sl << 16;
                 else pp[j / 2] = sl;
             }
@@ -1940,7 +1964,7 @@ struct BigLeaf {
             bsync();
 #pragma unroll
             for (int j = 0; j < BI; ++j) {
-                if (j * BT + tid < m) {
+                if ((unsigned)eidx(j, off) < (unsigned)m) {
                     PDQ_CHECK(mp(xs[j]) < (uint32_t)BBK, "leaf bucket");
                     PDQ_CHECK((cnt[mp(xs[j])] & 0xFFFFu) + ((pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu) < (uint32_t)m,
                               "leaf scatter slot");
