@@ -1321,7 +1321,9 @@ struct Sorter {
         mbar_wait(&sh.bar[st], (ci / B::NSTAGE) & 1u);
         ++ci;
         const long long q1 = clock64();
+#ifndef PDQ_BIG_PHASES
         if (tid == 0) sh.s_sch_claim += q1 - q0;  // (profiling) stage wait
+#endif
         unsigned lmask = 0, vmask = 0;
         int eqc = 0;
         if (lo_i == 0 && hi_i == TL)
@@ -1400,7 +1402,9 @@ struct Sorter {
         if (L && write_left) emit_run(kc, vc, dst, dstv, gl, aL, L, 1);
         if (R) emit_run(kc, vc, dst, dstv, gr, aR, R, 8);
         if (tid == 0) bulk_commit();
+#ifndef PDQ_BIG_PHASES
         if (tid == 0) sh.s_sch_idle += clock64() - q1;  // (profiling) whole tile after the stage wait
+#endif
     }
 
     // thread 0: keep NST tile loads in flight ahead of the compute side, walking the current task's
@@ -1618,6 +1622,24 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
 // removes the two deepest partition levels of a 2^28-key sort.
 #ifndef PDQ_BIG_SKIP
 #define PDQ_BIG_SKIP 0  // profiling builds only: 1 = no in-bucket ranking (output NOT sorted)
+#endif
+#ifdef PDQ_BIG_PHASES
+// profiling builds (tools/leaf_phases.py): thread 0 of k_base_big charges the cycles of leaf phase i to
+// one of the scheduler counters (k_sort's own uses of them are compiled out): 0 load + min/max,
+// 1 slots + scan, 2 scatter, 3 ranking + store
+#define PHASE_MARK(i)                                                                                  \
+    do {                                                                                               \
+        if (threadIdx.x == 0) {                                                                        \
+            const long long t_ = clock64();                                                            \
+            unsigned long long *c_[4] = {&sh.s_sch_retire, &sh.s_sch_claim, &sh.s_sch_fetch, &sh.s_sch_idle}; \
+            *c_[i] += t_ - pm;                                                                         \
+            pm = t_;                                                                                   \
+        }                                                                                              \
+    } while (0)
+#else
+#define PHASE_MARK(i) \
+    do {              \
+    } while (0)
 #endif
 template <bool FLOAT>
 struct BigLeaf {
@@ -1868,8 +1890,10 @@ struct BigLeaf {
         uint64_t cur = sh.lf[0];
         int k = 0;
         load(P, cur, xs);
+        long long pm = clock64();  // (PDQ_BIG_PHASES profiling builds)
         while (cur != NONE) {
             const long long c0 = clock64();
+            pm = c0;
             // thread 0 claims the next leaf; its descriptor stays in a register until the barrier before
             // the ranking phase, so the round trips never stall the barriers in between
             uint64_t pend = NONE;
@@ -1903,6 +1927,7 @@ struct BigLeaf {
                 red[96 + warp] = mx;
             }
             bsync();
+            PHASE_MARK(0);
             mn = __reduce_min_sync(0xffffffffu, red[64 + lane]);
             mx = __reduce_max_sync(0xffffffffu, red[96 + lane]);
             const U range = mx - mn;
@@ -1962,6 +1987,7 @@ struct BigLeaf {
                 for (int q = 0; q < PB / 4; ++q) c4[q] = make_uint4(cw[4 * q], cw[4 * q + 1], cw[4 * q + 2], cw[4 * q + 3]);
             }
             bsync();
+            PHASE_MARK(1);
 #pragma unroll
             for (int j = 0; j < BI; ++j) {
                 if ((unsigned)eidx(j, off) < (unsigned)m) {
@@ -1977,6 +2003,7 @@ struct BigLeaf {
                 sh.lf[k ^ 1] = pend;
             }
             bsync();
+            PHASE_MARK(2);
             const uint64_t nxt = sh.lf[k ^ 1];
             if (cmax <= (uint32_t)CMAX) {
                 load(P, nxt, xs);  // the next leaf's loads fly while this one is ranked and stored
@@ -2011,6 +2038,7 @@ struct BigLeaf {
                     sh.s_cyc_base += clock64() - c0;
                 }
             }
+            PHASE_MARK(3);
             cur = nxt;
             k ^= 1;
         }
@@ -2130,7 +2158,9 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
                 const long long c = clock64();
                 const unsigned old = atomicAdd(&P.segs[sid].tiles_done, t1 - t0);
                 sh.last = (old + (t1 - t0) == sh.seg.ntiles);
+#ifndef PDQ_BIG_PHASES
                 sh.s_sch_retire += clock64() - c;
+#endif
             }
             csync();
             if (sh.last) {

@@ -1,3 +1,5 @@
+"""Leaf-phase profile of k_base_big (build with tools/build_var.sh ph -DPDQ_BIG_PHASES, run with
+PDQ_LIB=tools/libvar_ph.so): share of thread-0 cycles per phase and cycles per leaf."""
 import sys
 sys.path.insert(0,'/root/repo')
 import torch
