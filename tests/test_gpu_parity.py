@@ -361,3 +361,18 @@ def test_host_pipeline_batches():
         HostPipeline(n, tdt, depth=3).sort(ins, outs)
         for x, y in zip(ins, outs):
             assert same_bytes(y.numpy(), oracle_sort(x.numpy())[0])
+
+
+@pytest.mark.parametrize("k", [1, 2, 16, 256])
+def test_device_counters_onk_bound(k):
+    # f1: the device counters re-assert the paper's O(nk) bound for k distinct keys
+    # (the reference's acceptance criterion counts partitions <= 2k) and a depth bound
+    n = 1 << 22
+    keys = workloads.c3(k, n)
+    got, _, st = gpu_sort(keys)
+    assert same_bytes(got, np.sort(keys))
+    assert st["partition_right_calls"] + st["partition_left_calls"] <= 2 * k + 2, st
+    assert st["max_depth"] <= 2 * 22, st
+    u = workloads.c1(n)
+    _, _, st = gpu_sort(u)
+    assert st["max_depth"] <= 2 * 22 and st["bad_partitions"] <= 4, st
