@@ -61,8 +61,9 @@ typedef struct pdq_config {
     int32_t use_break_patterns;       /* perturb child pivot samples after a bad split driver.py:62,239 */
     int32_t use_partial_insertion;    /* enables the sortedness check (K4) exits       driver.py:63,244 */
     /* ---- GPU fields ---- */
-    int32_t base_case_size;           /* K7 threshold, 1024..16384 (default 16384; clamped to 4096 for
-                                         8-byte keys and key-value sorts) */
+    int32_t base_case_size;           /* K7 threshold, 1024..32768 (default 32768), clamped to each
+                                         element type's base-case capacity: 24572 keys for 4-byte
+                                         keys without payload, 4096 otherwise */
     int32_t bad_budget;               /* -1: floor(log2 n) (driver.py:263); >= 0 overrides (0 forces the
                                          radix fallback on the first big segment: test knob) */
     int32_t reserved[4];              /* reserved[0] > 0: profiling knob, stop descending at that

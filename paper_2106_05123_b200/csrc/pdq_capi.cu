@@ -34,7 +34,7 @@ extern "C" void pdq_config_default(pdq_config *c) {
     c->use_partition_left = 1;
     c->use_break_patterns = 1;
     c->use_partial_insertion = 1;
-    c->base_case_size = 16384;
+    c->base_case_size = 32768;  // the largest leaf each element type's base-case kernel takes
     c->bad_budget = -1;
 }
 
@@ -49,8 +49,8 @@ extern "C" int pdq_config_validate(const pdq_config *c) {
     if (c->block_size < 1) return set_err(PDQ_ERR_CONFIG, "block_size must be >= 1%s");
     if (c->bad_partition_shift < 1) return set_err(PDQ_ERR_CONFIG, "bad_partition_shift must be >= 1%s");
     if (c->bad_partition_shift > 62) return set_err(PDQ_ERR_CONFIG, "bad_partition_shift must be <= 62%s");
-    if (c->base_case_size < 1024 || c->base_case_size > 16384)  // clamped per element type at launch
-        return set_err(PDQ_ERR_CONFIG, "base_case_size must be in [1024, 16384]%s");
+    if (c->base_case_size < 1024 || c->base_case_size > 32768)  // clamped per element type at launch
+        return set_err(PDQ_ERR_CONFIG, "base_case_size must be in [1024, 32768]%s");
     return PDQ_OK;
 }
 
@@ -114,7 +114,8 @@ struct LaunchInfo {
     int occ_base = 0;
 };
 
-// 4-byte keys without payload: 16K-key leaves sorted by k_base_big; other elements: 4K leaves (k_base)
+// 4-byte keys without payload: leaves of up to BIG_BASE - 4 (24572) keys sorted by k_base_big; other
+// elements: 4K leaves (k_base)
 template <class U, bool KV>
 constexpr bool big_leaves() {
     return sizeof(U) == 4 && !KV;

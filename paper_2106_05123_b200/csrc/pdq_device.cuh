@@ -20,7 +20,10 @@ constexpr int THREADS = 256;          // threads per CTA in every kernel
 constexpr int TILE = 4096;            // keys per partition tile (one "block" of partition.py:184)
 constexpr int ITEMS = TILE / THREADS; // keys per thread per tile
 constexpr int MAX_BASE = 4096;        // largest base-case segment (K7) for 8-byte and KV elements
-constexpr int BIG_BASE = 16384;       // largest base-case segment for 4-byte keys-only sorts (k_base_big)
+#ifndef PDQ_BIG_BASE
+#define PDQ_BIG_BASE 24576
+#endif
+constexpr int BIG_BASE = PDQ_BIG_BASE;  // base-case capacity for 4-byte keys-only sorts (k_base_big)
 constexpr int SAMPLES = 256;          // K1 pivot samples per big segment
 constexpr int WARPS = THREADS / 32;
 constexpr int64_t INLINE_FILL = 16 * TILE;  // fills up to this size run inline in the finalizer

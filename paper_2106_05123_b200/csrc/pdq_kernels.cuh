@@ -1607,8 +1607,8 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
     if (tid == 0) S::flush_counters(P);
 }
 
-// ---- K7 for 4-byte keys-only sorts: leaves of up to BIG_BASE = 16384 keys -----------------------------
-// One CTA of 1024 threads per SM; a leaf lives in registers (16 keys per thread) while it is bucketed:
+// ---- K7 for 4-byte keys-only sorts: leaves of up to BIG_BASE - 4 = 24572 keys ------------------------
+// One CTA of 1024 threads per SM; a leaf lives in registers (BIG_BASE / 1024 = 24 keys per thread) while it is bucketed:
 //   1. ordered image, block min/max; a constant leaf is already sorted (copied to A if it is in B);
 //   2. bucket(x) = hi32(((x - min) << clz(range)) * F), a monotone map onto 8192 buckets; a shared-memory
 //      atomic gives every key its slot, one block scan turns counts into (start, count) words;
@@ -1618,8 +1618,9 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
 // A leaf with a bucket larger than CMAX takes the slow path: such a bucket is accepted if it is
 // constant (repeated keys), otherwise the leaf is sorted by stable 8-bit LSD radix passes over
 // (key - min).  On the fast path the next leaf's loads fly while the current one is ranked.
-// Replaces insertion_sort / unguarded_insertion_sort (small_sorts.py:16-73) with a 16K-key leaf, which
-// removes the two deepest partition levels of a 2^28-key sort.
+// Replaces insertion_sort / unguarded_insertion_sort (small_sorts.py:16-73) with a 24K-key leaf, which
+// removes the two to three deepest partition levels of a 2^28-key sort (2^28 / 2^14 = 16384-key segments
+// are leaves whatever the sampling noise of their pivots).
 #ifndef PDQ_BIG_SKIP
 #define PDQ_BIG_SKIP 0  // profiling builds only: 1 = no in-bucket ranking (output NOT sorted)
 #endif
@@ -1646,6 +1647,7 @@ struct BigLeaf {
     using U = uint32_t;
     using O = Ord<U, FLOAT>;
     static constexpr int BT = 1024, BW = BT / 32, BI = BIG_BASE / BT;
+    static_assert(BIG_BASE % (4 * BT) == 0, "a leaf is read as 16-byte vectors: BIG_BASE = 4096 k");
 #ifndef PDQ_BIG_LOGBK
 #define PDQ_BIG_LOGBK 13
 #endif
@@ -1761,7 +1763,7 @@ struct BigLeaf {
     }
 
     // One stable 8-bit counting pass src -> dst over ((x - mn) >> shift) & 255 (ordered images); the
-    // final pass writes raw keys.  Warp w owns elements [512w, 512w + 512) in 16 rounds of 32; ranks
+    // final pass writes raw keys.  Warp w owns elements [32 BI w, 32 BI (w + 1)) in BI rounds of 32; ranks
     // within a warp from a ballot multisplit, per-warp 16-bit digit counters, one digit-major block scan.
     __device__ __forceinline__ static void radix_pass(const uint32_t *src, uint32_t *dst, int m, U mn, int shift,
                                                       bool fin) {
@@ -1772,10 +1774,10 @@ struct BigLeaf {
         reinterpret_cast<uint4 *>(wc)[lane] = make_uint4(0u, 0u, 0u, 0u);  // 256 counters
         __syncwarp();
         const unsigned ltm = lanemask_lt();
-        uint32_t rd[16];
+        uint32_t rd[BI];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int idx = warp * 512 + j * 32 + lane;
+        for (int j = 0; j < BI; ++j) {
+            const int idx = warp * (32 * BI) + j * 32 + lane;
             const bool valid = idx < m;
             const uint32_t d = valid ? ((src[idx] - mn) >> shift) & 255u : 0u;
             unsigned peers = __ballot_sync(0xffffffffu, valid);
@@ -1812,8 +1814,8 @@ struct BigLeaf {
         }
         bsync();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int idx = warp * 512 + j * 32 + lane;
+        for (int j = 0; j < BI; ++j) {
+            const int idx = warp * (32 * BI) + j * 32 + lane;
             if (idx < m) {
                 const uint32_t pos = (uint32_t)wc[rd[j] & 0xFFu] + (rd[j] >> 8);
                 const U x = src[idx];

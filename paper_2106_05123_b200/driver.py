@@ -60,7 +60,7 @@ class SortConfig:
     use_break_patterns: bool = True
     use_partial_insertion: bool = True
     # ---- GPU fields ----
-    base_case_size: int = 16384  # clamped to 4096 for 8-byte keys and key-value sorts
+    base_case_size: int = 32768  # clamped to each element type's base-case capacity
     bad_budget: int = -1
 
     def __post_init__(self):
@@ -77,8 +77,8 @@ class SortConfig:
             raise ValueError("bad_partition_shift must be >= 1")
         if self.bad_partition_shift > 62:
             raise ValueError("bad_partition_shift must be <= 62")
-        if not 1024 <= self.base_case_size <= 16384:
-            raise ValueError("base_case_size must be in [1024, 16384]")
+        if not 1024 <= self.base_case_size <= 32768:
+            raise ValueError("base_case_size must be in [1024, 32768]")
         if self.bad_budget < -1:
             raise ValueError("bad_budget must be -1 (log2 n) or >= 0")
 

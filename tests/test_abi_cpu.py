@@ -44,7 +44,7 @@ def test_config_struct_layout_and_defaults():
     L.pdq_config_default(ctypes.byref(c))
     assert (c.insertion_threshold, c.ninther_threshold, c.partial_insertion_budget, c.block_size,
             c.bad_partition_shift) == (24, 128, 8, 64, 3)  # driver.py:55-59
-    assert c.base_case_size == 16384 and c.bad_budget == -1
+    assert c.base_case_size == 32768 and c.bad_budget == -1
     assert ctypes.sizeof(_lib.PdqConfig) == 5 * 8 + 6 * 4 + 4 * 4
     mine = DEFAULT_CONFIG.to_c()
     assert bytes(mine) == bytes(c)

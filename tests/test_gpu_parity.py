@@ -72,7 +72,7 @@ def shapes(n, rng, dtype):
 
 
 SWEEP_SIZES = list(range(0, 65)) + [100, 1000, 1023, 1024, 1025, 4095, 4096, 4097, 8191, 8192, 10007,
-                                     16383, 16384, 16385, 32769, 65536, 100003, 1 << 20]
+                                     16383, 16384, 16385, 24571, 24572, 24573, 32769, 65536, 100003, 1 << 20]
 
 
 @pytest.mark.parametrize("dtype", DTYPES, ids=lambda d: np.dtype(d).name)
@@ -182,7 +182,7 @@ def test_forced_fallback_budget_zero(dtype):
     # bad_budget=0: the root starts with an exhausted budget, so it takes the K5 radix split
     # (driver.py:209-213 analogue); buckets resume quicksort with a fresh budget
     rng = np.random.default_rng(5)
-    for n in (20000, 300000, 1 << 22):  # above every base-case size (16384 for 4-byte keys)
+    for n in (30000, 300000, 1 << 22):  # above every base-case size (24572 for 4-byte keys)
         if dtype == "kv":
             keys = rng.integers(0, 50, n).astype(np.int64)
             vals = rng.integers(0, 2**32, n, dtype=np.uint32)
@@ -206,7 +206,7 @@ def test_big_leaf_slow_paths(dtype):
     rng = np.random.default_rng(11)
     big = np.iinfo(np.int32) if dtype == np.int32 else None
     lo, hi = (big.min, big.max) if big else (-np.inf, np.inf)
-    for n in (100, 5000, 12000, 16384):
+    for n in (100, 5000, 12000, 16384, 24572):
         k = rng.integers(0, 1000, n).astype(dtype)
         k[rng.choice(n, 6, replace=False)] = [lo, hi, lo, hi, 0, 1]
         got, _, _ = gpu_sort(k)

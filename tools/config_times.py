@@ -1,7 +1,7 @@
 """Device time of one sort for every BASELINE config case at full size (inputs resident in HBM,
 CUDA events around pdq_sort, median of 5 after 2 warm-ups).  Prints a markdown table.
 
-python tools/config_times.py
+python tools/config_times.py [case-prefix,...]
 """
 import statistics
 import sys
@@ -14,7 +14,10 @@ from paper_2106_05123_b200 import DeviceSorter, workloads  # noqa: E402
 
 print("| case | n | dtype | ms | Gkeys/s | partitions R/L | bad | fallbacks | leaves |")
 print("|---|---|---|---|---|---|---|---|---|")
+only = sys.argv[1].split(",") if len(sys.argv) > 1 else None
 for name, keys, vals in workloads.cases(0):
+    if only and not any(name.startswith(o) for o in only):
+        continue
     n = keys.size
     src = torch.from_numpy(keys).cuda()
     vsrc = None if vals is None else torch.from_numpy(vals.view(np.int32)).cuda()
