@@ -2049,6 +2049,298 @@ struct BigLeaf {
     }
 };
 
+// ---- K7 for 8-byte keys and key-value sorts: leaves of up to 8188 elements -------------------------
+// The design of BigLeaf for wider elements (1024 threads, 8 elements per thread, 4096 buckets):
+// elements compare as (ordered key, payload) pairs; the bucket map reads the key (or, for a leaf of
+// equal keys, the payload).  A bucket of more than CMAX elements is ranked by the same comparison loop
+// over the whole bucket (quadratic in the bucket, but only clustered leaves have such buckets).  Keys and
+// payloads leave by one TMA bulk store each.
+template <class U, bool FLOAT, bool KV>
+struct WideLeaf {
+    using O = Ord<U, FLOAT>;
+    using H = BigLeaf<false>;  // the 1024-thread block helpers
+    static constexpr int BT = 1024, BI = 8, CAP = BT * BI;
+    static constexpr int BBK = 4096, LOG_BK = 12;
+    static constexpr int KB = (CAP + 16) * (int)sizeof(U), VB = KV ? (CAP + 16) * 4 : 0;
+    static constexpr int KCK = 0, KCV = KB, KDK = KB + VB, KDV = 2 * KB + VB, CNT = 2 * KB + 2 * VB,
+                         RED = CNT + BBK * 4;
+    __host__ __device__ static constexpr int bytes() { return RED + 1024; }
+    __device__ __forceinline__ static U *kck() { return reinterpret_cast<U *>(g_dsm + KCK); }
+    __device__ __forceinline__ static uint32_t *kcv() { return reinterpret_cast<uint32_t *>(g_dsm + KCV); }
+    __device__ __forceinline__ static U *kdk() { return reinterpret_cast<U *>(g_dsm + KDK); }
+    __device__ __forceinline__ static uint32_t *kdv() { return reinterpret_cast<uint32_t *>(g_dsm + KDV); }
+    __device__ __forceinline__ static uint32_t *cnt() { return reinterpret_cast<uint32_t *>(g_dsm + CNT); }
+    __device__ __forceinline__ static uint64_t *red() { return reinterpret_cast<uint64_t *>(g_dsm + RED); }
+
+    // register j of thread t holds leaf element 4 ((j / 4) BT + t) + j % 4 - (b mod 4) (16-byte vectors)
+    __device__ __forceinline__ static int eidx(int j, int off) {
+        return 4 * ((j >> 2) * BT + (int)threadIdx.x) + (j & 3) - off;
+    }
+    __device__ __forceinline__ static void load(const Params &P, uint64_t lf, U (&xs)[BI], uint32_t (&vs)[BI]) {
+        const int tid = threadIdx.x;
+        const int m = lf == ~0ull ? 0 : (int)((lf >> 1) & 0x7FFF) + 1;
+        const int64_t b = (int64_t)(lf >> 16);
+        const int off = (int)(b & 3);
+        const U *src = (const U *)((lf & 1u) ? P.b_keys : P.a_keys) + (b - off);
+        const uint32_t *srcv = KV ? ((lf & 1u) ? P.b_vals : P.a_vals) + (b - off) : nullptr;
+        const int64_t room = P.n - (b - off);
+#pragma unroll
+        for (int jv = 0; jv < BI / 4; ++jv) {
+            const int e0 = 4 * (jv * BT + tid);
+            U k4[4] = {0, 0, 0, 0};
+            uint32_t v4[4] = {0, 0, 0, 0};
+            if (m > 0 && e0 < off + m && e0 + 4 > off) {
+                if (e0 + 4 <= room) {
+                    if constexpr (sizeof(U) == 4) {
+                        const uint4 y = __ldcg(reinterpret_cast<const uint4 *>(src + e0));
+                        k4[0] = (U)y.x; k4[1] = (U)y.y; k4[2] = (U)y.z; k4[3] = (U)y.w;
+                    } else {
+                        const ulonglong2 y0 = __ldcg(reinterpret_cast<const ulonglong2 *>(src + e0));
+                        const ulonglong2 y1 = __ldcg(reinterpret_cast<const ulonglong2 *>(src + e0 + 2));
+                        k4[0] = (U)y0.x; k4[1] = (U)y0.y; k4[2] = (U)y1.x; k4[3] = (U)y1.y;
+                    }
+                    if constexpr (KV) {
+                        const uint4 z = __ldcg(reinterpret_cast<const uint4 *>(srcv + e0));
+                        v4[0] = z.x; v4[1] = z.y; v4[2] = z.z; v4[3] = z.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (e0 + q < room) {
+                            k4[q] = ldcg(src + e0 + q);
+                            if constexpr (KV) v4[q] = ldcg(srcv + e0 + q);
+                        }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                xs[4 * jv + q] = k4[q];
+                vs[4 * jv + q] = v4[q];
+            }
+        }
+    }
+
+    __device__ __forceinline__ static bool less(U a, uint32_t va, U b, uint32_t vb) {
+        return a < b || (KV && a == b && va < vb);
+    }
+    __device__ __forceinline__ static U shfl_x(U x, int o) {
+        if constexpr (sizeof(U) == 4) return (U)__shfl_xor_sync(0xffffffffu, (uint32_t)x, o);
+        return (U)__shfl_xor_sync(0xffffffffu, (unsigned long long)x, o);
+    }
+
+    __device__ static void run(const Params &P) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        U *kc = kck(), *kd = kdk();
+        uint32_t *vc = kcv(), *vd = kdv(), *cn = cnt();
+        uint64_t *rd = red();
+        unsigned long long count = *(volatile unsigned long long *)&P.st->leaf_count;
+        if (count > P.leaf_cap) count = P.leaf_cap;
+        constexpr uint64_t NONE = ~0ull;
+        if (tid == 0) {
+            const unsigned long long idx = atomicAdd(&P.st->leaf_next, 1ull);
+            sh.lf[0] = idx < count ? ldcg(P.leaves + idx) : NONE;
+        }
+        H::bsync();
+        uint64_t cur = sh.lf[0];
+        int k = 0;
+        U xs[BI];
+        uint32_t vs[BI];
+        load(P, cur, xs, vs);
+        while (cur != NONE) {
+            const long long c0 = clock64();
+            uint64_t pend = NONE;
+            if (tid == 0) {
+                const unsigned long long idx = atomicAdd(&P.st->leaf_next, 1ull);
+                if (idx < count) pend = ldcg(P.leaves + idx);
+            }
+            const int m = (int)((cur >> 1) & 0x7FFF) + 1;
+            const int64_t b = (int64_t)(cur >> 16);
+            const bool srcB = cur & 1u;
+            const int off = (int)(b & 3);
+            reinterpret_cast<uint4 *>(cn)[tid] = make_uint4(0, 0, 0, 0);  // BBK = 4 BT counters
+            U kmn = ~(U)0, kmx = 0;
+            uint32_t vmn = 0xFFFFFFFFu, vmx = 0;
+#pragma unroll
+            for (int j = 0; j < BI; ++j) {
+                if ((unsigned)eidx(j, off) < (unsigned)m) {
+                    const U x = O::to(xs[j]);
+                    xs[j] = x;
+                    kmn = x < kmn ? x : kmn;
+                    kmx = x > kmx ? x : kmx;
+                    vmn = min(vmn, vs[j]);
+                    vmx = max(vmx, vs[j]);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const U a = shfl_x(kmn, o), c = shfl_x(kmx, o);
+                kmn = a < kmn ? a : kmn;
+                kmx = c > kmx ? c : kmx;
+            }
+            vmn = __reduce_min_sync(0xffffffffu, vmn);
+            vmx = __reduce_max_sync(0xffffffffu, vmx);
+            if (lane == 0) {
+                rd[warp] = (uint64_t)kmn;
+                rd[32 + warp] = (uint64_t)kmx;
+                rd[64 + warp] = vmn;
+                rd[96 + warp] = vmx;
+            }
+            H::bsync();
+            kmn = (U)rd[0];
+            kmx = (U)rd[32];
+            vmn = (uint32_t)rd[64];
+            vmx = (uint32_t)rd[96];
+            for (int q = 1; q < 32; ++q) {
+                const U a = (U)rd[q], c = (U)rd[32 + q];
+                kmn = a < kmn ? a : kmn;
+                kmx = c > kmx ? c : kmx;
+                vmn = min(vmn, (uint32_t)rd[64 + q]);
+                vmx = max(vmx, (uint32_t)rd[96 + q]);
+            }
+            const U krange = kmx - kmn;
+            if (krange == 0 && (!KV || vmn == vmx)) {
+                // a constant leaf is sorted; one in B is copied to its place in A
+                if (srcB) {
+                    U *a = (U *)P.a_keys + b;
+#pragma unroll
+                    for (int j = 0; j < BI; ++j)
+                        if ((unsigned)eidx(j, off) < (unsigned)m) {
+                            a[eidx(j, off)] = O::from(xs[j]);
+                            if constexpr (KV) P.a_vals[b + eidx(j, off)] = vs[j];
+                        }
+                }
+                if (tid == 0) {
+                    sh.lf[k ^ 1] = pend;
+                    sh.s_base++;
+                    sh.s_bytes += (srcB ? 2ull : 1ull) * (sizeof(U) + (KV ? 4 : 0)) * m;
+                    sh.s_cyc_base += clock64() - c0;
+                }
+                H::bsync();
+                cur = sh.lf[k ^ 1];
+                load(P, cur, xs, vs);
+                k ^= 1;
+                continue;
+            }
+            // bucket source: the key, or the payload when every key is equal
+            const bool by_key = krange != 0;
+            const uint64_t smn = by_key ? (uint64_t)kmn : (uint64_t)vmn;
+            const uint64_t srange = by_key ? (uint64_t)krange : (uint64_t)(vmx - vmn);
+            const int sh64 = __clzll((long long)srange);
+            const uint32_t ymax = (uint32_t)((srange << sh64) >> 32);
+            const uint32_t F = (uint32_t)__fdividef((float)(1ull << (32 + LOG_BK)), (float)ymax + 1.0f) - 2u;
+            auto bucket = [&](U x, uint32_t v) -> uint32_t {
+                const uint64_t d = (by_key ? (uint64_t)x : (uint64_t)v) - smn;
+                return __umulhi((uint32_t)((d << sh64) >> 32), F);
+            };
+            uint32_t pp[BI / 2];
+#pragma unroll
+            for (int j = 0; j < BI; ++j) {
+                const uint32_t sl =
+                    ((unsigned)eidx(j, off) < (unsigned)m) ? atomicAdd(&cn[bucket(xs[j], vs[j])], 1u) : 0u;
+                if (j & 1) pp[j / 2] |= sl << 16;
+                else pp[j / 2] = sl;
+            }
+            H::bsync();
+            {  // (start, count) words: thread t owns buckets [4t, 4t + 4)
+                uint4 *c4 = reinterpret_cast<uint4 *>(cn) + tid;
+                const uint4 y = *c4;
+                const uint32_t tot = y.x + y.y + y.z + y.w;
+                uint32_t run = H::block_excl_scan(tot, reinterpret_cast<uint32_t *>(rd) + 192);
+                uint4 w;
+                w.x = run | (y.x << 16); run += y.x;
+                w.y = run | (y.y << 16); run += y.y;
+                w.z = run | (y.z << 16); run += y.z;
+                w.w = run | (y.w << 16);
+                *c4 = w;
+            }
+            H::bsync();
+#pragma unroll
+            for (int j = 0; j < BI; ++j) {
+                if ((unsigned)eidx(j, off) < (unsigned)m) {
+                    const uint32_t pos = (cn[bucket(xs[j], vs[j])] & 0xFFFFu) + ((pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu);
+                    PDQ_CHECK(pos < (uint32_t)m, "wide leaf scatter slot");
+                    kc[pos] = xs[j];
+                    if constexpr (KV) vc[pos] = vs[j];
+                }
+            }
+            const int a0 = off;
+            if (tid == 0) {
+                bulk_wait_read();  // the previous leaf's bulk stores have left kd / vd
+                sh.lf[k ^ 1] = pend;
+            }
+            H::bsync();
+            const uint64_t nxt = sh.lf[k ^ 1];
+            load(P, nxt, xs, vs);  // the next leaf's loads fly while this one is ranked and stored
+#pragma unroll
+            for (int j = 0; j < BI; ++j) {
+                if (j * BT + tid < m) {
+                    const uint32_t p = j * BT + tid;
+                    const U x = kc[p];
+                    const uint32_t v = KV ? vc[p] : 0u;
+                    const uint32_t sc = cn[bucket(x, v)];
+                    const uint32_t s0 = sc & 0xFFFFu, e = s0 + (sc >> 16);
+                    uint32_t r = s0;
+                    for (uint32_t i = s0; i < e; ++i) {  // ranks among the bucket ((key, payload) order)
+                        const U y = kc[i];
+                        const uint32_t w = KV ? vc[i] : 0u;
+                        r += less(y, w, x, v) | ((y == x) & (w == v) & (i < p));
+                    }
+                    PDQ_CHECK(r < (uint32_t)m, "wide leaf rank");
+                    kd[a0 + r] = O::from(x);
+                    if constexpr (KV) vd[a0 + r] = v;
+                }
+            }
+            fence_proxy_async();
+            H::bsync();
+            {  // kd/vd[a0, a0 + m) -> A[b, b + m): 16-byte bodies by bulk stores, head/tail by threads
+                U *a = (U *)P.a_keys + b;
+                uint32_t *av = KV ? P.a_vals + b : nullptr;
+                int h = (4 - a0) & 3;
+                if (h > m) h = m;
+                const int nb = ((m - h) / 4) * 4;
+                if (tid > 0 && tid < 4 && tid - 1 < h) {
+                    a[tid - 1] = kd[a0 + tid - 1];
+                    if constexpr (KV) av[tid - 1] = vd[a0 + tid - 1];
+                }
+                if (tid >= 4 && tid < 8 && h + nb + tid - 4 < m) {
+                    a[h + nb + tid - 4] = kd[a0 + h + nb + tid - 4];
+                    if constexpr (KV) av[h + nb + tid - 4] = vd[a0 + h + nb + tid - 4];
+                }
+                if (tid == 0) {
+                    if (nb) {
+                        bulk_s2g(a + h, kd + a0 + h, (unsigned)(nb * sizeof(U)));
+                        if constexpr (KV) bulk_s2g(av + h, vd + a0 + h, (unsigned)nb * 4u);
+                    }
+                    bulk_commit();
+                    sh.s_base++;
+                    sh.s_bytes += 2ull * (sizeof(U) + (KV ? 4 : 0)) * m;
+                    sh.s_cyc_base += clock64() - c0;
+                }
+            }
+            cur = nxt;
+            k ^= 1;
+        }
+        if (tid == 0) bulk_wait_all();
+        H::bsync();
+    }
+};
+
+template <class U, bool FLOAT, bool KV>
+__global__ void __launch_bounds__(1024, 1) k_base_wide(const __grid_constant__ Params P) {
+    using S = Sorter<U, FLOAT, KV>;
+    Shared &sh = g_sh;
+    const int tid = threadIdx.x;
+    if (ld_volatile_u32(&P.st->reverse)) return;
+    if (tid == 0) S::zero_counters();
+    WideLeaf<U, FLOAT, KV>::run(P);
+    if (tid == 0) {
+        atomicAdd(&P.st->c_bytes_base, sh.s_bytes);
+        sh.s_bytes = 0;
+        S::flush_counters(P);
+    }
+}
+
 template <bool FLOAT>
 __global__ void __launch_bounds__(BigLeaf<FLOAT>::BT, 1) k_base_big(const __grid_constant__ Params P) {
     using S = Sorter<uint32_t, FLOAT, false>;
