@@ -114,11 +114,8 @@ struct LaunchInfo {
     int occ_base = 0;
 };
 
-#ifndef PDQ_WIDE_LEAVES
-#define PDQ_WIDE_LEAVES 1  // 8-byte keys and key-value sorts: 8188-element leaves (k_base_wide), else 4K (k_base)
-#endif
-// 4-byte keys without payload: leaves of up to BIG_BASE - 4 (24572) keys sorted by k_base_big; other
-// elements: 4K leaves (k_base)
+// 4-byte keys without payload: leaves of up to BIG_BASE - 4 (24572) keys sorted by k_base_big; 8-byte
+// keys and key-value sorts: leaves of up to 8188 elements sorted by k_base_wide
 template <class U, bool KV>
 constexpr bool big_leaves() {
     return sizeof(U) == 4 && !KV;
@@ -153,19 +150,11 @@ cudaError_t prepare(LaunchInfo &li) {
             if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached.occ_base, k_base_big<FLOAT>, BigLeaf<FLOAT>::BT,
                                                                    BigLeaf<FLOAT>::bytes())) != cudaSuccess)
                 return e;
-        } else if constexpr (PDQ_WIDE_LEAVES) {
+        } else {
             if ((e = cudaFuncSetAttribute(k_base_wide<U, FLOAT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           WideLeaf<U, FLOAT, KV>::bytes())) != cudaSuccess)
                 return e;
             cached.occ_base = 1;
-        } else {
-            const int smb = BaseBufs<U, KV>::bytes();
-            if ((e = cudaFuncSetAttribute(k_base<U, FLOAT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb)) !=
-                cudaSuccess)
-                return e;
-            if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached.occ_base, k_base<U, FLOAT, KV>, THREADS,
-                                                                   smb)) != cudaSuccess)
-                return e;
         }
         if (cached.occ_base < 1) cached.occ_base = 1;
         if ((e = cudaDeviceGetAttribute(&cached.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
@@ -183,7 +172,7 @@ template <class U, bool FLOAT, bool KV>
 int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEvent_t ev1) {
     LaunchInfo li;
     // (k_base_big reads a leaf as 16-byte vectors from its aligned base: up to 3 slots of lead-in)
-    const int base_max = big_leaves<U, KV>() ? BIG_BASE - 4 : (PDQ_WIDE_LEAVES ? WideLeaf<U, FLOAT, KV>::CAP - 4 : MAX_BASE);
+    const int base_max = big_leaves<U, KV>() ? BIG_BASE - 4 : WideLeaf<U, FLOAT, KV>::CAP - 4;
     if (P.base_size > base_max) P.base_size = base_max;
     cudaError_t e = prepare<U, FLOAT, KV>(li);
     if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "setup: %s", cudaGetErrorString(e));
@@ -208,10 +197,8 @@ int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEven
     if (ev1) cudaEventRecord(ev1, s);
     if constexpr (big_leaves<U, KV>())
         k_base_big<FLOAT><<<(unsigned)(li.sms * li.occ_base), BigLeaf<FLOAT>::BT, BigLeaf<FLOAT>::bytes(), s>>>(P);
-    else if constexpr (PDQ_WIDE_LEAVES)
-        k_base_wide<U, FLOAT, KV><<<(unsigned)li.sms, 1024, WideLeaf<U, FLOAT, KV>::bytes(), s>>>(P);
     else
-        k_base<U, FLOAT, KV><<<(unsigned)(li.sms * li.occ_base), THREADS, BaseBufs<U, KV>::bytes(), s>>>(P);
+        k_base_wide<U, FLOAT, KV><<<(unsigned)li.sms, 1024, WideLeaf<U, FLOAT, KV>::bytes(), s>>>(P);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "launch: %s", cudaGetErrorString(e));
     return PDQ_OK;

@@ -19,7 +19,6 @@ namespace pdq {
 constexpr int THREADS = 256;          // threads per CTA in every kernel
 constexpr int TILE = 4096;            // keys per partition tile (one "block" of partition.py:184)
 constexpr int ITEMS = TILE / THREADS; // keys per thread per tile
-constexpr int MAX_BASE = 4096;        // largest base-case segment (K7) for 8-byte and KV elements
 #ifndef PDQ_BIG_BASE
 #define PDQ_BIG_BASE 24576
 #endif

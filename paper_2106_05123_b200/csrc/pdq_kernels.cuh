@@ -2,22 +2,23 @@
 //
 //   K1 sample pivot          spawn(): 64 (256 for >= 2^20 keys) stratified samples, warp/CTA
 //                            bitonic, median (generalises choose_pivot, driver.py:81-113)
-//   K2 partition_right       part_tile(): TMA bulk tile -> classify -> block scan -> one packed
-//                            atomic per tile for both sides -> shared-memory compaction -> 16 B
-//                            stores (block_partition_right, partition.py:184-301)
+//   K2 partition_right       part_tile(): TMA bulk tile -> classify -> per-warp counts -> one packed
+//                            reservation atomic per tile for both sides -> warp-ballot compaction in
+//                            shared memory -> TMA bulk stores (block_partition_right, partition.py:184-301)
 //   K3 partition_left        part_tile() in I_LEFT mode (partition.py:128-181, driver.py:222-225)
 //   K4 sortedness check      k_check(): adjacent-compare reduction; k_sort prologue reverses
 //                            non-increasing input (partial_insertion_sort path, driver.py:244-250)
 //   K5 bad-partition budget  finalize_part(): is_bad_partition (driver.py:116-124), budget,
 //                            sample perturbation (break_patterns, driver.py:127-156); an exhausted
 //                            budget switches the segment to radix exchange (heapsort's role)
-//   K6 segment queue         k_sort(): persistent CTAs claim chunks of 8 tiles from a device ring of
-//                            64-bit task words, prefetch the next tile by TMA while storing the
-//                            current one, retire chunks with one fence + counter; the last chunk's
-//                            CTA finalizes the segment and spawns its children (driver.py:198-260)
-//   K7 base case             k_base() / leaf_loop(): leaves <= base_case_size sorted by a one-pass
-//                            bucket sort + per-thread insertion runs, radix passes for clustered
-//                            leaves (insertion_sort / unguarded_insertion_sort, small_sorts.py:16-73)
+//   K6 segment queue         k_sort(): persistent CTAs claim chunks of up to 32 tiles from a device ring
+//                            of 64-bit task words, keep two TMA tile loads in flight, retire chunks
+//                            with one bulk-store wait + fence + counter; the last chunk's CTA
+//                            finalizes the segment and spawns its children (driver.py:198-260)
+//   K7 base case             k_base_big (4-byte keys, leaves <= 24572) / k_base_wide (8-byte keys and
+//                            key-value sorts, leaves <= 8188): bucket placement + in-bucket ranking in
+//                            shared memory, tiny segments by one warp in registers (insertion_sort /
+//                            unguarded_insertion_sort, small_sorts.py:16-73)
 #pragma once
 
 #include "pdq_device.cuh"
@@ -36,18 +37,6 @@ __device__ __forceinline__ uint32_t task_end_tile(uint32_t first, uint32_t N, ui
 #define PDQ_NST 1
 #endif
 constexpr int NST = PDQ_NST;            // TMA stages: tile loads run up to NST tiles ahead of compute
-constexpr int RADIX_BITS = 8;
-constexpr int RADIX_DIGITS = 1 << RADIX_BITS;
-constexpr int CNT_BYTES = RADIX_DIGITS * WARPS * 2;  // per-warp u16 digit counters
-#ifndef PDQ_BUCKET_BITS
-#define PDQ_BUCKET_BITS 11
-#endif
-#ifndef PDQ_KB_SKIP
-#define PDQ_KB_SKIP 0
-#endif
-constexpr int BUCKET_MAX = 24;  // larger buckets (clustered / repeated keys): radix passes instead
-constexpr int RUN_MAX = 64;     // longest per-thread insertion run (8 buckets) accepted
-
 // CTA barrier (named barrier 1, all THREADS threads)
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(THREADS) : "memory"); }
 __device__ __forceinline__ int csync_or(int p) {
@@ -148,30 +137,10 @@ struct Bufs {
     __host__ __device__ static constexpr int bytes() { return KEY_BYTES + VAL_BYTES; }
 };
 
-// Dynamic shared memory of the base-case kernel: two ping-pong buffers and the radix counters.
-template <class U, bool KV>
-struct BaseBufs {
-    static constexpr int KEY_BYTES = 2 * MAX_BASE * (int)sizeof(U);
-    static constexpr int VAL_BYTES = KV ? 2 * MAX_BASE * 4 : 0;
-    __device__ __forceinline__ static U *kx() { return reinterpret_cast<U *>(g_dsm); }
-    __device__ __forceinline__ static U *kc() { return reinterpret_cast<U *>(g_dsm) + MAX_BASE; }
-    __device__ __forceinline__ static uint32_t *vx() { return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES); }
-    __device__ __forceinline__ static uint32_t *vc() {
-        return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES) + MAX_BASE;
-    }
-    __device__ __forceinline__ static uint16_t *cnt() { return reinterpret_cast<uint16_t *>(g_dsm + KEY_BYTES + VAL_BYTES); }
-    __device__ __forceinline__ static uint32_t *bkt() { return reinterpret_cast<uint32_t *>(g_dsm + KEY_BYTES + VAL_BYTES); }
-    // K7 bucket count: 4096 for 4-byte keys, 2048 for wider elements (keeps 2 CTAs/SM there)
-    static constexpr int BK = 1 << ((sizeof(U) == 4 && !KV) ? PDQ_BUCKET_BITS : 11);
-    static constexpr int CNT_AREA = CNT_BYTES > BK * 4 ? CNT_BYTES : BK * 4;
-    __host__ __device__ static constexpr int bytes() { return KEY_BYTES + VAL_BYTES + CNT_AREA; }
-};
-
 template <class U, bool FLOAT, bool KV>
 struct Sorter {
     using O = Ord<U, FLOAT>;
     using B = Bufs<U, KV>;
-    using BB = BaseBufs<U, KV>;
     static constexpr int VEC = 16 / sizeof(U);
     static constexpr int AL = KV ? 4 : VEC;  // element alignment making both key and payload 16 B aligned
     static constexpr int ELEM_BYTES = sizeof(U) + (KV ? 4 : 0);
@@ -317,406 +286,9 @@ struct Sorter {
         atomicExch(&P.st->done, 1u);
     }
 
-    // ---- K7: base case, range-reduced LSD radix sort in shared memory ---------------------
-    // One stable 4-bit counting pass (per-thread u16 counters, CUB-style) per 4 bits of
-    // (max - min) over the segment's ordered keys: a 4K-key leaf of a uniform int32 sort
-    // spans ~2^16 values, i.e. 4 passes.  KV segments whose keys repeat get payload passes
-    // first so equal keys end up ordered by payload (the tuple order).
-    template <class T>
-    __device__ __forceinline__ static void ld16(const T *s, int base, T (&x)[ITEMS]) {
-        if constexpr (sizeof(T) == 4) {
-            const uint4 *p = reinterpret_cast<const uint4 *>(s + base);
-#pragma unroll
-            for (int q = 0; q < ITEMS / 4; ++q) {
-                const uint4 y = p[q];
-                x[4 * q] = (T)y.x;
-                x[4 * q + 1] = (T)y.y;
-                x[4 * q + 2] = (T)y.z;
-                x[4 * q + 3] = (T)y.w;
-            }
-        } else {
-            const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(s + base);
-#pragma unroll
-            for (int q = 0; q < ITEMS / 2; ++q) {
-                const ulonglong2 y = p[q];
-                x[2 * q] = (T)y.x;
-                x[2 * q + 1] = (T)y.y;
-            }
-        }
-    }
-
-    // One stable 8-bit counting pass.  Warp w owns elements [512w, 512w+512) in 16 rounds of 32
-    // (element 512w + 32j + lane), so (warp, round, lane) is the element order.  Within a round,
-    // __match_any_sync groups equal digits; each group's rank continues the warp's running count
-    // for that digit (per-warp u16 counters in shared memory, updated by the group leader).  One
-    // block-wide scan over (digit, warp) turns the counts into output offsets.
-    __device__ __noinline__ static void radix_pass(const U *ks, const uint32_t *vs, U *kd, uint32_t *vd, int m,
-                                                   U mn, int shift, bool on_vals, uint32_t vmn) {
-        Shared &sh = g_sh;
-        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-        uint16_t *wc = BB::cnt() + warp * RADIX_DIGITS;
-        uint32_t *wc32 = reinterpret_cast<uint32_t *>(wc);
-#pragma unroll
-        for (int i = lane; i < RADIX_DIGITS / 2; i += 32) wc32[i] = 0;
-        __syncwarp();
-        const unsigned ltm = lanemask_lt();
-        const int wbase = warp * (32 * ITEMS);
-        uint32_t rd[ITEMS];  // (rank within the warp's digit run) << 8 | digit; keys are re-read later
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-            const int idx = wbase + j * 32 + lane;
-            const bool valid = idx < m;
-            const U kk = valid ? ks[idx] : (U)0;
-            const uint32_t vv = (KV && valid) ? vs[idx] : 0u;
-            const uint32_t d = on_vals ? ((vv - vmn) >> shift) & (RADIX_DIGITS - 1)
-                                       : (uint32_t)((kk - mn) >> shift) & (RADIX_DIGITS - 1);
-            // peers = lanes with the same digit (warp multisplit over the digit's bits: ballots are
-            // full-rate, match.any is not); invalid lanes match no valid lane
-            unsigned peers = __ballot_sync(0xffffffffu, valid);
-            peers = valid ? peers : ~peers;
-#pragma unroll
-            for (int bit = 0; bit < RADIX_BITS; ++bit) {
-                const bool on = (d >> bit) & 1u;
-                const unsigned bb = __ballot_sync(0xffffffffu, on);
-                peers &= on ? bb : ~bb;
-            }
-            // the group continues the warp's running count for digit d; its leader advances it
-            const uint32_t before = valid ? (uint32_t)wc[d] : 0u;
-            const uint32_t r = (uint32_t)__popc(peers & ltm);
-            __syncwarp();
-            if (valid && r == 0) wc[d] = (uint16_t)(before + __popc(peers));
-            __syncwarp();
-            rd[j] = ((before + r) << 8) | d;
-        }
-        csync();
-        // digit-major exclusive scan: thread t owns digit t across the warps
-        {
-            uint32_t c[WARPS], tot = 0;
-#pragma unroll
-            for (int w = 0; w < WARPS; ++w) {
-                c[w] = BB::cnt()[w * RADIX_DIGITS + tid];
-                tot += c[w];
-            }
-            uint32_t inc = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += y;
-            }
-            if (lane == 31) sh.scan[warp] = inc;
-            csync();
-            uint32_t run = inc - tot;
-#pragma unroll
-            for (int q = 0; q < WARPS; ++q) run += (q < warp) ? sh.scan[q] : 0u;
-#pragma unroll
-            for (int w = 0; w < WARPS; ++w) {
-                BB::cnt()[w * RADIX_DIGITS + tid] = (uint16_t)run;
-                run += c[w];
-            }
-        }
-        csync();
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-            const int idx = wbase + j * 32 + lane;
-            if (idx < m) {
-                const uint32_t pos = (uint32_t)wc[rd[j] & 0xFFu] + (rd[j] >> 8);
-                kd[pos] = ks[idx];
-                if (KV) vd[pos] = vs[idx];
-            }
-        }
-        csync();
-    }
-
-    __device__ __forceinline__ static U shfl_xor_u(U x, int o) {
-        if (sizeof(U) == 4) return (U)__shfl_xor_sync(0xffffffffu, (uint32_t)x, o);
-        return (U)__shfl_xor_sync(0xffffffffu, (unsigned long long)x, o);
-    }
     __device__ __forceinline__ static int clz_u(U x) {
         if (sizeof(U) == 4) return __clz((uint32_t)x);
         return __clzll((long long)x);
-    }
-
-    __device__ __forceinline__ static U *kbuf(int c) { return c ? BB::kc() : BB::kx(); }
-    __device__ __forceinline__ static uint32_t *vbuf(int c) { return KV ? (c ? BB::vc() : BB::vx()) : nullptr; }
-
-    // Radix path of the leaf sort (kx/vx hold the leaf): stable 8-bit LSD passes over (key - mn); a KV
-    // leaf with repeated keys first orders by payload.  Returns the buffer index holding the result.
-    __device__ __noinline__ static int radix_leaf(int m, U mn, U range, uint32_t vmn, uint32_t vmx) {
-        const int tid = threadIdx.x;
-        const int kbits = range ? (int)(sizeof(U) * 8) - clz_u(range) : 0;
-        int c = 0;
-        for (int s = 0; s < kbits; s += RADIX_BITS, c ^= 1)
-            radix_pass(kbuf(c), vbuf(c), kbuf(c ^ 1), vbuf(c ^ 1), m, mn, s, false, 0);
-        if (KV && vmx != vmn) {
-            // keys repeat? then order equal keys by payload: payload passes, then key passes again
-            int dup = 0;
-            const U *ck = kbuf(c);
-            for (int i = tid; i + 1 < m; i += THREADS) dup |= (ck[i] == ck[i + 1]);
-            if (csync_or(dup)) {
-                const int vbits = 32 - __clz(vmx - vmn);
-                for (int s = 0; s < vbits; s += RADIX_BITS, c ^= 1)
-                    radix_pass(kbuf(c), vbuf(c), kbuf(c ^ 1), vbuf(c ^ 1), m, mn, s, true, vmn);
-                for (int s = 0; s < kbits; s += RADIX_BITS, c ^= 1)
-                    radix_pass(kbuf(c), vbuf(c), kbuf(c ^ 1), vbuf(c ^ 1), m, mn, s, false, 0);
-            }
-        }
-        return c;
-    }
-
-    // Issue the register loads of one leaf (descriptor lf; ~0 = none): thread t gets elements t + 256 j.
-    __device__ __forceinline__ static void load_leaf(const Params &P, uint64_t lf, U (&xs)[ITEMS],
-                                                     uint32_t (&vs)[KV ? ITEMS : 1]) {
-        const int tid = threadIdx.x;
-        const int m = lf == ~0ull ? 0 : (int)((lf >> 1) & 0x7FFF) + 1;
-        const int64_t b = (int64_t)(lf >> 16);
-        const U *src = (const U *)((lf & 1u) ? P.b_keys : P.a_keys);
-        const uint32_t *srcv = (lf & 1u) ? P.b_vals : P.a_vals;
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-            const int i = j * THREADS + tid;
-            xs[j] = i < m ? ldcg(src + b + i) : (U)0;
-            if constexpr (KV) vs[j] = i < m ? ldcg(srcv + b + i) : 0u;
-        }
-    }
-
-    // K7 leaf sort (segment of m <= 4096 keys).  The leaf is loaded into registers (16 keys per thread,
-    // all loads in flight at once) and range-reduced to [mn, mn + range].  Fast path, a one-pass bucket
-    // sort: a monotone scaling of (key - mn) picks one of 2048 buckets, a shared-memory atomic gives
-    // every key its slot in its bucket, one scan turns counts into bucket offsets and the keys go
-    // straight from registers to their bucket in kc.  Thread t's buckets [8t, 8t + 8) form one
-    // contiguous run of kc that is already ordered between buckets, so one insertion sort of the run
-    // (ordering (key, payload) pairs) finishes the leaf.  A 2.8K-key leaf of a uniform sort has ~1.4
-    // keys per bucket: about one warp instruction per key, instead of one radix pass per 8 key bits.
-    // When a bucket holds more than BUCKET_MAX keys or a run exceeds RUN_MAX (clustered or repeated
-    // keys), the leaf goes through the stable 8-bit radix passes instead.
-    // The leaf loop is software-pipelined: a leaf's keys are loaded into registers while the previous
-    // leaf is insertion-sorted and stored, and thread 0 claims the following leaf (one atomic on the leaf
-    // queue + one descriptor load) while the current one is bucketed.
-    __device__ __noinline__ static void leaf_loop(const Params &P) {
-        Shared &sh = g_sh;
-        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-        uint32_t *cnt = BB::bkt();
-        unsigned long long count = *(volatile unsigned long long *)&P.st->leaf_count;
-        if (count > P.leaf_cap) count = P.leaf_cap;
-        constexpr uint64_t NONE = ~0ull;
-        auto claim = [&](int k) {
-            if (tid == 0) {
-                const unsigned long long idx = atomicAdd(&P.st->leaf_next, 1ull);
-                sh.lf[k] = idx < count ? ldcg(P.leaves + idx) : NONE;
-            }
-        };
-        U xs[ITEMS];
-        uint32_t vs[KV ? ITEMS : 1];
-        claim(0);
-        csync();
-        uint64_t cur = sh.lf[0];
-        int k = 0;
-        load_leaf(P, cur, xs, vs);
-        while (cur != NONE) {
-        const long long c0 = clock64();
-        claim(k ^ 1);
-        const int m = (int)((cur >> 1) & 0x7FFF) + 1;
-        const int64_t b = (int64_t)(cur >> 16);
-        const int J = (m + THREADS - 1) / THREADS;
-        {  // zero the bucket counters while the loads are in flight
-            uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
-#pragma unroll
-            for (int q = 0; q < BB::BK / 4 / THREADS; ++q) c4[q * THREADS + tid] = make_uint4(0, 0, 0, 0);
-        }
-        // ordered image, min/max of keys and payload
-        U mn = ~(U)0, mx = 0;
-        uint32_t vmn = 0xFFFFFFFFu, vmx = 0;
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-            if (j < J && j * THREADS + tid < m) {
-                const U x = O::to(xs[j]);
-                xs[j] = x;
-                mn = x < mn ? x : mn;
-                mx = x > mx ? x : mx;
-                if constexpr (KV) {
-                    vmn = vs[j] < vmn ? vs[j] : vmn;
-                    vmx = vs[j] > vmx ? vs[j] : vmx;
-                }
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const U a = shfl_xor_u(mn, o), c = shfl_xor_u(mx, o);
-            mn = a < mn ? a : mn;
-            mx = c > mx ? c : mx;
-            if (KV) {
-                const uint32_t a2 = __shfl_xor_sync(0xffffffffu, vmn, o), c2 = __shfl_xor_sync(0xffffffffu, vmx, o);
-                vmn = a2 < vmn ? a2 : vmn;
-                vmx = c2 > vmx ? c2 : vmx;
-            }
-        }
-        if (lane == 0) {
-            sh.red_min[warp] = (uint64_t)mn;
-            sh.red_max[warp] = (uint64_t)mx;
-            if (KV) {
-                sh.red_a[warp] = vmn;
-                sh.red_b[warp] = vmx;
-            }
-        }
-        csync();
-        mn = (U)sh.red_min[0];
-        mx = (U)sh.red_max[0];
-        if (KV) {
-            vmn = sh.red_a[0];
-            vmx = sh.red_b[0];
-        }
-#pragma unroll
-        for (int q = 1; q < WARPS; ++q) {
-            const U a = (U)sh.red_min[q], c = (U)sh.red_max[q];
-            mn = a < mn ? a : mn;
-            mx = c > mx ? c : mx;
-            if (KV) {
-                vmn = sh.red_a[q] < vmn ? sh.red_a[q] : vmn;
-                vmx = sh.red_b[q] > vmx ? sh.red_b[q] : vmx;
-            }
-        }
-        const U range = mx - mn;
-        bool ok = range != 0;  // uniform across the CTA
-#if PDQ_KB_SKIP == 2  // profiling build only: leaf copied unsorted (measures the load/store floor)
-        ok = false;
-#endif
-        // bucket(x) = floor(y * BUCKETS / (ry + 1)), y = (x - mn) >> s0 fitting 32 bits: monotone in x
-        const int s0 = (sizeof(U) == 8 && (uint64_t)range >> 32) ? 32 - __clz((uint32_t)((uint64_t)range >> 32)) : 0;
-        // (R from a float quotient, no division subroutine; rounding only shifts bucket edges, the clamp
-        // keeps the last bucket in range, and a constant factor keeps the map monotone)
-        const uint64_t R = (uint64_t)__fdividef((float)((uint64_t)BB::BK << 32), (float)(uint32_t)(range >> s0) + 1.0f);
-        auto bucket = [&](U x) -> uint32_t {
-            return min((uint32_t)(((uint64_t)(uint32_t)((x - mn) >> s0) * R) >> 32), (uint32_t)BB::BK - 1);
-        };
-        uint32_t slot[ITEMS / 2];  // two 16-bit bucket slots per register
-        int r0 = 0, r1 = 0;        // this thread's run [r0, r1) of kc
-        if (ok) {
-#pragma unroll
-            for (int j = 0; j < ITEMS; ++j) {
-                uint32_t sl = 0;
-                if (j < J && j * THREADS + tid < m) sl = atomicAdd(&cnt[bucket(xs[j])], 1u);
-                if (j & 1) slot[j / 2] |= sl << 16;
-                else slot[j / 2] = sl;
-            }
-            csync();
-            // exclusive scan of the bucket counts (thread t owns buckets [8t, 8t + 8)); largest bucket/run
-            constexpr int PER = BB::BK / THREADS;
-            uint32_t c[PER], tot = 0, big = 0;
-            const uint4 *c4 = reinterpret_cast<const uint4 *>(cnt + PER * tid);
-#pragma unroll
-            for (int q = 0; q < PER / 4; ++q) {
-                const uint4 y = c4[q];
-                c[4 * q] = y.x; c[4 * q + 1] = y.y; c[4 * q + 2] = y.z; c[4 * q + 3] = y.w;
-            }
-#pragma unroll
-            for (int q = 0; q < PER; ++q) { tot += c[q]; big = c[q] > big ? c[q] : big; }
-            uint32_t inc = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += y;
-            }
-            big = __reduce_max_sync(0xffffffffu, big | (tot > (uint32_t)RUN_MAX ? 0x10000u : 0u));
-            if (lane == 31) { sh.scan[warp] = inc; sh.red_a[warp] = big; }
-            csync();
-            uint32_t run = inc - tot;
-            big = 0;
-#pragma unroll
-            for (int q = 0; q < WARPS; ++q) {
-                run += (q < warp) ? sh.scan[q] : 0u;
-                big = sh.red_a[q] > big ? sh.red_a[q] : big;
-            }
-            ok = big <= (uint32_t)BUCKET_MAX;
-            r0 = (int)run;
-            r1 = (int)(run + tot);
-            uint4 *w4 = reinterpret_cast<uint4 *>(cnt + PER * tid);
-#pragma unroll
-            for (int q = 0; q < PER / 4; ++q) {
-                uint4 y;
-                y.x = run; run += c[4 * q];
-                y.y = run; run += c[4 * q + 1];
-                y.z = run; run += c[4 * q + 2];
-                y.w = run; run += c[4 * q + 3];
-                w4[q] = y;
-            }
-            csync();
-        }
-        int c = 0;  // index of the buffer holding the current order (0: kx/vx, 1: kc/vc)
-        const uint64_t nxt = sh.lf[k ^ 1];  // written by thread 0 before the first barrier above
-        if (ok) {
-            U *kc = BB::kc();
-            uint32_t *vc = BB::vc();
-#pragma unroll
-            for (int j = 0; j < ITEMS; ++j) {
-                if (j < J && j * THREADS + tid < m) {
-                    const uint32_t pos = cnt[bucket(xs[j])] + ((slot[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
-                    kc[pos] = xs[j];
-                    if constexpr (KV) vc[pos] = vs[j];
-                }
-            }
-            csync();
-            load_leaf(P, nxt, xs, vs);  // the next leaf's loads fly while this one is insertion-sorted and stored
-            // insertion sort of this thread's run (elements only move inside their bucket); `top` is
-            // the largest element of the sorted prefix, so an element already in place costs one compare
-            if (PDQ_KB_SKIP != 1 && r1 > r0) {  // (PDQ_KB_SKIP=1: profiling build, no insertion)
-                U top = kc[r0];
-                uint32_t vtop = KV ? vc[r0] : 0u;
-                for (int i = r0 + 1; i < r1; ++i) {
-                    const U x = kc[i];
-                    const uint32_t v = KV ? vc[i] : 0u;
-                    bool before = x < top;
-                    if constexpr (KV) before |= (x == top) && v < vtop;
-                    if (!before) {
-                        top = x;
-                        vtop = v;
-                        continue;
-                    }
-                    kc[i] = top;
-                    if (KV) vc[i] = vtop;
-                    int j = i - 1;
-                    for (; j > r0; --j) {
-                        const U y = kc[j - 1];
-                        bool gt = y > x;
-                        if constexpr (KV) gt |= (y == x) && vc[j - 1] > v;
-                        if (!gt) break;
-                        kc[j] = y;
-                        if (KV) vc[j] = vc[j - 1];
-                    }
-                    kc[j] = x;
-                    if (KV) vc[j] = v;
-                }
-            }
-            c = 1;
-        } else {
-#pragma unroll
-            for (int j = 0; j < ITEMS; ++j) {
-                const int i = j * THREADS + tid;
-                if (j < J && i < m) {
-                    BB::kx()[i] = xs[j];
-                    if constexpr (KV) BB::vx()[i] = vs[j];
-                }
-            }
-            csync();
-            c = PDQ_KB_SKIP == 2 ? 0 : radix_leaf(m, mn, range, vmn, vmx);
-            load_leaf(P, nxt, xs, vs);  // (after the call: nothing of the leaf loop lives across it)
-        }
-        csync();
-        const U *fk = kbuf(c);
-        store_lin<U>((U *)P.a_keys + b, m, [&](int i) { return O::from(fk[i]); });
-        if (KV) {
-            const uint32_t *fv = vbuf(c);
-            store_lin<uint32_t>(P.a_vals + b, m, [&](int i) { return fv[i]; });
-        }
-        csync();
-        if (tid == 0) {
-            sh.s_base++;
-            sh.s_bytes += 2ull * ELEM_BYTES * m;
-            sh.s_cyc_base += clock64() - c0;
-        }
-        cur = nxt;
-        k ^= 1;
-        }
-        csync();
     }
 
     // <= 64 keys: warp 0 sorts them in registers (2 per lane, bitonic over shuffles) straight into A.
@@ -2349,32 +1921,6 @@ __global__ void __launch_bounds__(BigLeaf<FLOAT>::BT, 1) k_base_big(const __grid
     if (ld_volatile_u32(&P.st->reverse)) return;
     if (tid == 0) S::zero_counters();
     BigLeaf<FLOAT>::run(P);
-    if (tid == 0) {
-        atomicAdd(&P.st->c_bytes_base, sh.s_bytes);
-        sh.s_bytes = 0;
-        S::flush_counters(P);
-    }
-}
-
-// ---- K7: the base-case kernel: persistent CTAs sort the queued leaves ---------------------------------
-#ifndef PDQ_BASE_MINB
-#define PDQ_BASE_MINB 4
-#endif
-// 4 CTAs/SM leave 64 registers per thread: the leaf's 16 keys per thread stay in registers
-template <class U, bool KV>
-constexpr int base_min_blocks() {
-    constexpr int fit = (228 * 1024) / (BaseBufs<U, KV>::bytes() + 2304);  // + static smem + reserve
-    return fit < PDQ_BASE_MINB ? (fit < 1 ? 1 : fit) : PDQ_BASE_MINB;
-}
-template <class U, bool FLOAT, bool KV>
-__global__ void __launch_bounds__(THREADS, base_min_blocks<U, KV>()) k_base(const __grid_constant__ Params P) {
-    using S = Sorter<U, FLOAT, KV>;
-    Shared &sh = g_sh;
-    const int tid = threadIdx.x;
-    if (ld_volatile_u32(&P.st->reverse)) return;
-    if (tid == 0) S::zero_counters();
-    S::leaf_loop(P);
-    csync();
     if (tid == 0) {
         atomicAdd(&P.st->c_bytes_base, sh.s_bytes);
         sh.s_bytes = 0;
