@@ -1633,6 +1633,7 @@ struct WideLeaf {
     using H = BigLeaf<false>;  // the 1024-thread block helpers
     static constexpr int BT = 1024, BI = 8, CAP = BT * BI;
     static constexpr int BBK = 4096, LOG_BK = 12;
+    static constexpr int CMAX = 32;  // largest bucket ranked by comparisons; beyond it the leaf takes radix passes
     static constexpr int KB = (CAP + 16) * (int)sizeof(U), VB = KV ? (CAP + 16) * 4 : 0;
     static constexpr int KCK = 0, KCV = KB, KDK = KB + VB, KDV = 2 * KB + VB, CNT = 2 * KB + 2 * VB,
                          RED = CNT + BBK * 4;
@@ -1698,6 +1699,100 @@ struct WideLeaf {
     __device__ __forceinline__ static U shfl_x(U x, int o) {
         if constexpr (sizeof(U) == 4) return (U)__shfl_xor_sync(0xffffffffu, (uint32_t)x, o);
         return (U)__shfl_xor_sync(0xffffffffu, (unsigned long long)x, o);
+    }
+
+    // One stable 8-bit counting pass over digit ((payload or key) - base) >> shift: warp w owns elements
+    // [256w, 256w + 256) in 8 rounds of 32, ranks from a ballot multisplit, per-warp 16-bit counters,
+    // one digit-major block scan.  The final pass writes raw keys to kd/vd at a0.
+    __device__ __forceinline__ static void radix_pass(const U *sk, const uint32_t *sv, U *dk, uint32_t *dv, int m,
+                                                      bool on_vals, uint64_t base, int shift, bool fin) {
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        uint16_t *wc16 = reinterpret_cast<uint16_t *>(cnt());
+        uint16_t *wc = wc16 + warp * 256;
+        uint32_t *scr = reinterpret_cast<uint32_t *>(red()) + 128;
+        reinterpret_cast<uint4 *>(wc)[lane] = make_uint4(0u, 0u, 0u, 0u);  // 256 counters
+        __syncwarp();
+        const unsigned ltm = lanemask_lt();
+        uint32_t rdg[BI];
+#pragma unroll
+        for (int j = 0; j < BI; ++j) {
+            const int idx = warp * (32 * BI) + j * 32 + lane;
+            const bool valid = idx < m;
+            const uint64_t src = valid ? (on_vals ? (uint64_t)sv[idx] : (uint64_t)sk[idx]) : 0ull;
+            const uint32_t d = valid ? (uint32_t)((src - base) >> shift) & 255u : 0u;
+            unsigned peers = __ballot_sync(0xffffffffu, valid);
+            peers = valid ? peers : ~peers;
+#pragma unroll
+            for (int bit = 0; bit < 8; ++bit) {
+                const bool on = (d >> bit) & 1u;
+                const unsigned bb = __ballot_sync(0xffffffffu, on);
+                peers &= on ? bb : ~bb;
+            }
+            const uint32_t before = valid ? (uint32_t)wc[d] : 0u;
+            const uint32_t r = (uint32_t)__popc(peers & ltm);
+            __syncwarp();
+            if (valid && r == 0) wc[d] = (uint16_t)(before + __popc(peers));
+            __syncwarp();
+            rdg[j] = ((before + r) << 8) | d;
+        }
+        H::bsync();
+        {  // digit-major scan over (digit, warp): thread t owns digit t >> 2, warps 8 (t & 3) .. + 8
+            const int d = tid >> 2, w0 = 8 * (tid & 3);
+            uint32_t c[8], tot = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                c[q] = wc16[(w0 + q) * 256 + d];
+                tot += c[q];
+            }
+            uint32_t run = H::block_excl_scan(tot, scr);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                wc16[(w0 + q) * 256 + d] = (uint16_t)run;
+                run += c[q];
+            }
+        }
+        H::bsync();
+#pragma unroll
+        for (int j = 0; j < BI; ++j) {
+            const int idx = warp * (32 * BI) + j * 32 + lane;
+            if (idx < m) {
+                const uint32_t pos = (uint32_t)wc[rdg[j] & 0xFFu] + (rdg[j] >> 8);
+                const U x = sk[idx];
+                dk[pos] = fin ? O::from(x) : x;
+                if constexpr (KV) dv[pos] = sv[idx];
+            }
+        }
+        H::bsync();
+    }
+    // kc/vc[0, m) -> kd/vd[a0 + i] in (key, payload) order: LSD passes over the payload digits, then
+    // the key digits (both range-reduced); the final pass reads kc and writes kd
+    __device__ __noinline__ static void radix_leaf(int m, int a0, U kmn, U krange, uint32_t vmn, uint32_t vrange) {
+        U *kc = kck(), *kd = kdk();
+        uint32_t *vc = kcv(), *vd = kdv();
+        const int vb = (KV && vrange) ? 32 - __clz(vrange) : 0;
+        const int kb = krange ? 8 * (int)sizeof(U) - (sizeof(U) == 4 ? __clz((uint32_t)krange) : __clzll((long long)krange)) : 0;
+        const int npv = (vb + 7) / 8, npk = (kb + 7) / 8, np = npv + npk;
+        const U *sk = kc;
+        const uint32_t *sv = vc;
+        U *dk = kd;
+        uint32_t *dv = vd;
+        if ((np & 1) == 0) {  // the final pass must read kc and write kd
+            for (int i = threadIdx.x; i < m; i += BT) {
+                kd[i] = kc[i];
+                if constexpr (KV) vd[i] = vc[i];
+            }
+            H::bsync();
+            sk = kd; sv = vd; dk = kc; dv = vc;
+        }
+        for (int q = 0; q < np; ++q) {
+            const bool fin = q == np - 1, on_vals = q < npv;
+            radix_pass(sk, sv, fin ? kd + a0 : dk, fin ? vd + a0 : dv, m, on_vals, on_vals ? (uint64_t)vmn : (uint64_t)kmn,
+                       8 * (on_vals ? q : q - npv), fin);
+            const U *tk = sk;
+            const uint32_t *tv = sv;
+            sk = dk; sv = dv;
+            dk = const_cast<U *>(tk); dv = const_cast<uint32_t *>(tv);
+        }
     }
 
     __device__ static void run(const Params &P) {
@@ -1814,11 +1909,13 @@ struct WideLeaf {
                 else pp[j / 2] = sl;
             }
             H::bsync();
+            uint32_t cmax;
             {  // (start, count) words: thread t owns buckets [4t, 4t + 4)
                 uint4 *c4 = reinterpret_cast<uint4 *>(cn) + tid;
                 const uint4 y = *c4;
                 const uint32_t tot = y.x + y.y + y.z + y.w;
-                uint32_t run = H::block_excl_scan(tot, reinterpret_cast<uint32_t *>(rd) + 192);
+                const uint32_t mc = max(max(y.x, y.y), max(y.z, y.w));
+                uint32_t run = H::block_excl_scan(tot, reinterpret_cast<uint32_t *>(rd) + 128, mc, &cmax);
                 uint4 w;
                 w.x = run | (y.x << 16); run += y.x;
                 w.y = run | (y.y << 16); run += y.y;
@@ -1843,6 +1940,11 @@ struct WideLeaf {
             }
             H::bsync();
             const uint64_t nxt = sh.lf[k ^ 1];
+            if (cmax > (uint32_t)CMAX) {
+                // clustered leaf (typically many equal keys with distinct payloads): stable radix passes
+                radix_leaf(m, a0, kmn, krange, vmn, vmx - vmn);
+                load(P, nxt, xs, vs);
+            } else {
             load(P, nxt, xs, vs);  // the next leaf's loads fly while this one is ranked and stored
 #pragma unroll
             for (int j = 0; j < BI; ++j) {
@@ -1862,6 +1964,7 @@ struct WideLeaf {
                     kd[a0 + r] = O::from(x);
                     if constexpr (KV) vd[a0 + r] = v;
                 }
+            }
             }
             fence_proxy_async();
             H::bsync();
