@@ -376,3 +376,20 @@ def test_device_counters_onk_bound(k):
     u = workloads.c1(n)
     _, _, st = gpu_sort(u)
     assert st["max_depth"] <= 2 * 22 and st["bad_partitions"] <= 4, st
+
+
+@pytest.mark.parametrize("k", [2, 16, 1024])
+def test_kv_low_cardinality_argsort(k):
+    # argsort by a low-cardinality key (distinct payloads = indices): key-value leaves whose buckets hold
+    # many equal keys take k_base_wide's radix fallback; the (key, payload) order is exact
+    rng = np.random.default_rng(100 + k)
+    n = (1 << 20) + 3
+    keys = (rng.integers(0, k, n).astype(np.int64) << 30) - (1 << 40)
+    vals = rng.permutation(n).astype(np.uint32)
+    got_k, got_v, _ = gpu_sort(keys, vals)
+    exp_k, exp_v = workloads.expected(keys, vals)
+    assert same_bytes(got_k, exp_k) and same_bytes(got_v, exp_v)
+    k32 = (keys >> 30).astype(np.int32)  # 4-byte keys with a payload (8-byte elements)
+    got_k, got_v, _ = gpu_sort(k32, vals)
+    exp_k, exp_v = workloads.expected(k32, vals)
+    assert same_bytes(got_k, exp_k) and same_bytes(got_v, exp_v)
