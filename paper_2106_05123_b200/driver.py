@@ -397,16 +397,36 @@ def sort(data: MutableSequence, config: SortConfig = DEFAULT_CONFIG, *, values=N
 
 
 def sort_with(data: MutableSequence, lt: Ordering, branch_cheap: bool = False) -> None:
-    """Sort ``data`` in place under ``lt`` (driver.py:273-279).  The device path
-    implements the built-in ordering only: ``lt`` must be ``operator.lt``."""
+    """Sort ``data`` in place under ``lt`` (driver.py:273-279).  The device path implements the
+    built-in orderings: ``operator.lt`` (ascending) and ``operator.gt`` (descending)."""
     sort_with_config(data, lt, DEFAULT_CONFIG, branch_cheap=branch_cheap)
+
+
+def _reverse_in_place(data) -> None:
+    import torch
+
+    if isinstance(data, torch.Tensor):
+        data.copy_(data.flip(0))
+    elif isinstance(data, np.ndarray):
+        data[...] = data[::-1].copy()
+    else:  # list, array.array, any MutableSequence
+        data.reverse()
 
 
 def sort_with_config(data: MutableSequence, lt: Ordering, config: SortConfig,
                      branch_cheap: Optional[bool] = None) -> None:
-    """Sort ``data`` in place under ``lt`` with explicit tunables (driver.py:282-292)."""
-    if lt is not operator.lt:
-        raise NotImplementedError(
-            "the B200 sort path implements the built-in ordering (operator.lt) only; "
-            "custom Python orderings have no device equivalent and there is no CPU fallback")
-    _sort_any(data, config)
+    """Sort ``data`` in place under ``lt`` with explicit tunables (driver.py:282-292).
+
+    ``operator.gt`` sorts descending: the ascending device sort, reversed.  Equal elements are
+    bit-identical (keys) or identical tuples ((key, payload) pairs), so the descending output is the
+    unique one the reference produces under ``gt``."""
+    if lt is operator.lt:
+        _sort_any(data, config)
+        return
+    if lt is operator.gt:
+        _sort_any(data, config)
+        _reverse_in_place(data)
+        return
+    raise NotImplementedError(
+        "the B200 sort path implements the built-in orderings (operator.lt, operator.gt) only; "
+        "custom Python orderings have no device equivalent and there is no CPU fallback")

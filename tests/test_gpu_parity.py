@@ -393,3 +393,27 @@ def test_kv_low_cardinality_argsort(k):
     got_k, got_v, _ = gpu_sort(k32, vals)
     exp_k, exp_v = workloads.expected(k32, vals)
     assert same_bytes(got_k, exp_k) and same_bytes(got_v, exp_v)
+
+
+def test_sort_with_descending_ordering():
+    # f4: operator.gt (descending) runs on the device as the ascending sort reversed; the output is the
+    # unique descending order, as the reference's sort_with(data, operator.gt) produces
+    import operator
+
+    rng = np.random.default_rng(31)
+    ints = rng.integers(-(2**31), 2**31, 50001).tolist()
+    w = list(ints)
+    sort_with(w, operator.gt)
+    assert w == sorted(ints, reverse=True)
+    flts = rng.standard_normal(30001).tolist()
+    w = list(flts)
+    sort_with(w, operator.gt)
+    assert w == sorted(flts, reverse=True)
+    pairs = list(zip(rng.integers(0, 100, 20001).tolist(), rng.permutation(20001).tolist()))
+    w = list(pairs)
+    sort_with(w, operator.gt)
+    assert w == sorted(pairs, reverse=True)
+    t = torch.from_numpy(rng.integers(-1000, 1000, 70001).astype(np.int32)).to(DEV)
+    ref = np.sort(t.cpu().numpy())[::-1]
+    sort_with(t, operator.gt)
+    assert same_bytes(t.cpu().numpy(), ref.copy())
