@@ -124,6 +124,25 @@ int pdq_sort_ex(void *keys, int dtype, uint32_t *payload, int64_t n, const pdq_c
  * `workspace` into *stats (may be NULL) and return its status. */
 int pdq_sort_finish(void *workspace, pdq_stats *stats, void *stream);
 
+/* ---- multi-GPU sample sort: bucketing one rank's shard ----
+ * No reference counterpart (the reference is single-process); the host side is
+ * paper_2106_05123_b200/distributed.py:sample_sort. */
+
+/* Bytes of device workspace pdq_bucket() needs for n elements and nbuckets (<= 64) buckets. */
+size_t pdq_bucket_workspace_bytes(int64_t n, int nbuckets);
+
+/* Split the n elements (keys + optional uint32 payload) of a shard whose first element has global
+ * index gidx_base into nbuckets = nsplit + 1 buckets.  Splitters are nsplit ascending
+ * (key, payload, global index) triples in device memory (split_payload may be NULL without a
+ * payload); element i goes to bucket b = number of splitters below (key_i, payload_i,
+ * gidx_base + i), keys compared in the sort's order.  out_keys / out_payload (device, n elements)
+ * receive the elements grouped by bucket, stable within a bucket; bucket_counts (device,
+ * int64[nbuckets]) each bucket's size.  Asynchronous on `stream`. */
+int pdq_bucket(const void *keys, int dtype, const uint32_t *payload, int64_t n, int64_t gidx_base,
+               const void *split_keys, const uint32_t *split_payload, const int64_t *split_gidx,
+               int nsplit, void *out_keys, uint32_t *out_payload, int64_t *bucket_counts,
+               void *workspace, size_t workspace_bytes, void *stream);
+
 /* Thread-local message for the last error returned on this thread. */
 const char *pdq_last_error(void);
 

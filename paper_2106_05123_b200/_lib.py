@@ -39,6 +39,8 @@ EXPORTS = (
     "pdq_sort_finish",
     "pdq_last_error",
     "pdq_version",
+    "pdq_bucket_workspace_bytes",
+    "pdq_bucket",
 )
 
 
@@ -140,6 +142,10 @@ def lib() -> ctypes.CDLL:
             L.pdq_sort_ex.restype = I
             L.pdq_sort_finish.argtypes = [P, ctypes.POINTER(PdqStats), P]
             L.pdq_sort_finish.restype = I
+            L.pdq_bucket_workspace_bytes.argtypes = [I64, I]
+            L.pdq_bucket_workspace_bytes.restype = SZ
+            L.pdq_bucket.argtypes = [P, I, P, I64, I64, P, P, P, I, P, P, P, P, SZ, P]
+            L.pdq_bucket.restype = I
             L.pdq_last_error.argtypes = []
             L.pdq_last_error.restype = ctypes.c_char_p
             L.pdq_version.argtypes = []

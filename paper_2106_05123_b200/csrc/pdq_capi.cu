@@ -9,6 +9,7 @@
 #include <mutex>
 
 #include "../../include/pdq_b200.h"
+#include "pdq_bucket.cuh"
 #include "pdq_kernels.cuh"
 
 using namespace pdq;
@@ -317,4 +318,66 @@ extern "C" int pdq_sort_finish(void *workspace, pdq_stats *out, void *stream) {
     if (st.status == -8) return set_err(PDQ_ERR_INTERNAL, "device watchdog: the task queue stalled for 10 s%s");
     if (st.status) return set_err(PDQ_ERR_INTERNAL, "device-side failure (descriptor capacity)%s");
     return PDQ_OK;
+}
+
+// ---- sample-sort bucketing ----------------------------------------
+
+extern "C" size_t pdq_bucket_workspace_bytes(int64_t n, int nbuckets) {
+    if (n < 0 || nbuckets < 1 || nbuckets > BK_MAX) return 0;
+    return a256((size_t)nbuckets * (size_t)bucket_geom(n).warps() * sizeof(int64_t));
+}
+
+namespace {
+template <class U, bool FLOAT, bool KV>
+int launch_bucket(const void *keys, const uint32_t *vals, int64_t n, int64_t gidx_base, const void *sk,
+                  const uint32_t *sv, const int64_t *sg, int ns, void *ok, uint32_t *ov, int64_t *bucket_counts,
+                  int64_t *cnt, cudaStream_t s) {
+    const BucketGeom g = bucket_geom(n);
+    const int nb = ns + 1;
+    k_bucket_count<U, FLOAT, KV><<<g.ctas, BK_THREADS, 0, s>>>((const U *)keys, vals, n, gidx_base, (const U *)sk,
+                                                               sv, sg, ns, cnt, g);
+    k_bucket_scan<<<1, BK_SCAN_THREADS, 0, s>>>(cnt, (int64_t)nb * g.warps(), nb, g.warps(), bucket_counts);
+    k_bucket_scatter<U, FLOAT, KV><<<g.ctas, BK_THREADS, 0, s>>>((const U *)keys, vals, n, gidx_base,
+                                                                 (const U *)sk, sv, sg, ns, cnt, (U *)ok, ov, g);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "bucket launch: %s", cudaGetErrorString(e));
+    return PDQ_OK;
+}
+}  // namespace
+
+extern "C" int pdq_bucket(const void *keys, int dtype, const uint32_t *payload, int64_t n, int64_t gidx_base,
+                          const void *split_keys, const uint32_t *split_payload, const int64_t *split_gidx,
+                          int nsplit, void *out_keys, uint32_t *out_payload, int64_t *bucket_counts,
+                          void *workspace, size_t ws_bytes, void *stream) {
+    if (dtype_size(dtype) == 0) return set_err(PDQ_ERR_DTYPE, "unsupported dtype code%s");
+    if (n < 0) return set_err(PDQ_ERR_ARG, "n must be >= 0%s");
+    if (nsplit < 0 || nsplit + 1 > BK_MAX) return set_err(PDQ_ERR_ARG, "nsplit must be in [0, 63]%s");
+    if (!bucket_counts) return set_err(PDQ_ERR_ARG, "bucket_counts is NULL%s");
+    if (n > 0 && (!keys || !out_keys)) return set_err(PDQ_ERR_ARG, "keys / out_keys is NULL%s");
+    if ((payload == nullptr) != (out_payload == nullptr))
+        return set_err(PDQ_ERR_ARG, "payload and out_payload must both be given or both be NULL%s");
+    if (nsplit > 0 && (!split_keys || !split_gidx || (payload && !split_payload)))
+        return set_err(PDQ_ERR_ARG, "splitter arrays are NULL%s");
+    const size_t need = pdq_bucket_workspace_bytes(n, nsplit + 1);
+    if (!workspace || ws_bytes < need) return set_err(PDQ_ERR_WORKSPACE, "bucket workspace too small%s");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0) {
+        cudaError_t e = cudaMemsetAsync(bucket_counts, 0, (size_t)(nsplit + 1) * sizeof(int64_t), s);
+        return e == cudaSuccess ? PDQ_OK : set_err(PDQ_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
+    }
+    int64_t *cnt = (int64_t *)workspace;
+    const bool kv = payload != nullptr;
+#define PDQ_BK(U, F) \
+    (kv ? launch_bucket<U, F, true>(keys, payload, n, gidx_base, split_keys, split_payload, split_gidx, nsplit, \
+                                    out_keys, out_payload, bucket_counts, cnt, s)                              \
+        : launch_bucket<U, F, false>(keys, payload, n, gidx_base, split_keys, split_payload, split_gidx, nsplit, \
+                                     out_keys, out_payload, bucket_counts, cnt, s))
+    switch (dtype) {
+        case PDQ_I32: return PDQ_BK(uint32_t, false);
+        case PDQ_F32: return PDQ_BK(uint32_t, true);
+        case PDQ_I64: return PDQ_BK(uint64_t, false);
+        case PDQ_F64: return PDQ_BK(uint64_t, true);
+    }
+#undef PDQ_BK
+    return set_err(PDQ_ERR_DTYPE, "unsupported dtype code%s");
 }
