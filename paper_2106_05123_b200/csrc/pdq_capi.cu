@@ -324,24 +324,47 @@ extern "C" int pdq_sort_finish(void *workspace, pdq_stats *out, void *stream) {
 
 extern "C" size_t pdq_bucket_workspace_bytes(int64_t n, int nbuckets) {
     if (n < 0 || nbuckets < 1 || nbuckets > BK_MAX) return 0;
-    return a256((size_t)nbuckets * (size_t)bucket_geom(n).warps() * sizeof(int64_t));
+    return a256((size_t)nbuckets * (size_t)bucket_geom(n).ctas * sizeof(int64_t));
 }
 
 namespace {
-template <class U, bool FLOAT, bool KV>
+template <class U, bool FLOAT, bool KV, int LT>
 int launch_bucket(const void *keys, const uint32_t *vals, int64_t n, int64_t gidx_base, const void *sk,
                   const uint32_t *sv, const int64_t *sg, int ns, void *ok, uint32_t *ov, int64_t *bucket_counts,
                   int64_t *cnt, cudaStream_t s) {
     const BucketGeom g = bucket_geom(n);
     const int nb = ns + 1;
-    k_bucket_count<U, FLOAT, KV><<<g.ctas, BK_THREADS, 0, s>>>((const U *)keys, vals, n, gidx_base, (const U *)sk,
-                                                               sv, sg, ns, cnt, g);
-    k_bucket_scan<<<1, BK_SCAN_THREADS, 0, s>>>(cnt, (int64_t)nb * g.warps(), nb, g.warps(), bucket_counts);
-    k_bucket_scatter<U, FLOAT, KV><<<g.ctas, BK_THREADS, 0, s>>>((const U *)keys, vals, n, gidx_base,
-                                                                 (const U *)sk, sv, sg, ns, cnt, (U *)ok, ov, g);
+    const size_t hist = (size_t)nb * BK_THREADS * sizeof(uint32_t);
+    const size_t sc = sizeof(ScatterSmem<U, KV>) + hist;
+    cudaFuncSetAttribute(k_bucket_count<U, FLOAT, KV, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(BK_MAX * BK_THREADS * sizeof(uint32_t)));
+    cudaFuncSetAttribute(k_bucket_scatter<U, FLOAT, KV, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(ScatterSmem<U, KV>) + BK_MAX * BK_THREADS * sizeof(uint32_t)));
+    k_bucket_count<U, FLOAT, KV, LT><<<g.ctas, BK_THREADS, hist, s>>>((const U *)keys, vals, n, gidx_base,
+                                                                         (const U *)sk, sv, sg, ns, cnt, g);
+    k_bucket_scan<<<1, BK_SCAN_THREADS, 0, s>>>(cnt, (int64_t)nb * g.ctas, nb, g.ctas, bucket_counts);
+    k_bucket_scatter<U, FLOAT, KV, LT><<<g.ctas, BK_THREADS, sc, s>>>(
+        (const U *)keys, vals, n, gidx_base, (const U *)sk, sv, sg, ns, cnt, (U *)ok, ov, g);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "bucket launch: %s", cudaGetErrorString(e));
     return PDQ_OK;
+}
+
+template <class U, bool FLOAT, bool KV>
+int launch_bucket_nb(const void *keys, const uint32_t *vals, int64_t n, int64_t gidx_base, const void *sk,
+                     const uint32_t *sv, const int64_t *sg, int ns, void *ok, uint32_t *ov, int64_t *bucket_counts,
+                     int64_t *cnt, cudaStream_t s) {
+    // up to 8 buckets (one NVLink node): per-thread counts packed in registers, the splitter search
+    // unrolled to its depth
+#define PDQ_LB(LT) launch_bucket<U, FLOAT, KV, LT>(keys, vals, n, gidx_base, sk, sv, sg, ns, ok, ov, bucket_counts, cnt, s)
+    switch (bucket_log2(ns + 1)) {
+        case 0: return PDQ_LB(0);
+        case 1: return PDQ_LB(1);
+        case 2: return PDQ_LB(2);
+        case 3: return PDQ_LB(3);
+        default: return PDQ_LB(-1);
+    }
+#undef PDQ_LB
 }
 }  // namespace
 
@@ -365,12 +388,14 @@ extern "C" int pdq_bucket(const void *keys, int dtype, const uint32_t *payload, 
         cudaError_t e = cudaMemsetAsync(bucket_counts, 0, (size_t)(nsplit + 1) * sizeof(int64_t), s);
         return e == cudaSuccess ? PDQ_OK : set_err(PDQ_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
     }
+    if (((uintptr_t)keys & 15) || ((uintptr_t)payload & 15))
+        return set_err(PDQ_ERR_ALIGN, "keys and payload must be 16-byte aligned%s");
     int64_t *cnt = (int64_t *)workspace;
     const bool kv = payload != nullptr;
 #define PDQ_BK(U, F) \
-    (kv ? launch_bucket<U, F, true>(keys, payload, n, gidx_base, split_keys, split_payload, split_gidx, nsplit, \
+    (kv ? launch_bucket_nb<U, F, true>(keys, payload, n, gidx_base, split_keys, split_payload, split_gidx, nsplit, \
                                     out_keys, out_payload, bucket_counts, cnt, s)                              \
-        : launch_bucket<U, F, false>(keys, payload, n, gidx_base, split_keys, split_payload, split_gidx, nsplit, \
+        : launch_bucket_nb<U, F, false>(keys, payload, n, gidx_base, split_keys, split_payload, split_gidx, nsplit, \
                                      out_keys, out_payload, bucket_counts, cnt, s))
     switch (dtype) {
         case PDQ_I32: return PDQ_BK(uint32_t, false);
