@@ -25,10 +25,18 @@
 namespace pdq {
 
 constexpr int BK_THREADS = 256;
-constexpr int BK_IPT = 16;                       // elements per thread per tile
-constexpr int BK_TILE = BK_THREADS * BK_IPT;     // 4096
 constexpr int BK_MAX = 64;                       // buckets (ranks) per call
-constexpr int BK_MAX_CTAS = 148 * 4;
+constexpr int BK_MAX_CTAS = 148 * 8;             // upper bound of every element type's grid
+
+// Per element type: elements per thread per tile (4-byte keys: 16, wider elements: 8, which keeps
+// them in registers without spilling) and the CTAs per SM the registers allow.
+template <class U, bool KV>
+struct BkShape {
+    static constexpr int IPT = (sizeof(U) == 4 && !KV) ? 16 : 8;
+    static constexpr int TILE = BK_THREADS * IPT;
+    static constexpr int MINB = IPT == 16 ? 3 : 4;
+    static constexpr int CTAS = 148 * 2 * MINB;
+};
 constexpr int BK_SCAN_THREADS = 1024;
 
 struct BucketGeom {
@@ -36,11 +44,11 @@ struct BucketGeom {
     int64_t per_cta;    // elements per CTA range (whole tiles)
 };
 
-__host__ __device__ inline BucketGeom bucket_geom(int64_t n) {
+__host__ __device__ inline BucketGeom bucket_geom(int64_t n, int tile, int max_ctas) {
     BucketGeom g;
-    int64_t tiles = (n + BK_TILE - 1) / BK_TILE;
-    g.ctas = (int)(tiles < 1 ? 1 : (tiles > BK_MAX_CTAS ? BK_MAX_CTAS : tiles));
-    g.per_cta = ((tiles + g.ctas - 1) / g.ctas) * BK_TILE;
+    int64_t tiles = (n + tile - 1) / tile;
+    g.ctas = (int)(tiles < 1 ? 1 : (tiles > max_ctas ? max_ctas : tiles));
+    g.per_cta = ((tiles + g.ctas - 1) / g.ctas) * tile;
     return g;
 }
 
@@ -52,6 +60,8 @@ __host__ __device__ inline int bucket_log2(int nb) {  // splitter table of 2^L -
 
 template <class U, bool FLOAT, bool KV>
 struct Bucketer {
+    static constexpr int BK_IPT = BkShape<U, KV>::IPT;
+    static constexpr int BK_TILE = BkShape<U, KV>::TILE;
     struct Split {
         U sk[BK_MAX];
         uint32_t sv[BK_MAX];
@@ -171,12 +181,13 @@ struct Bucketer {
 
 // Pass 1: per-CTA bucket counts, stored bucket-major: cnt[b * ctas + cta].
 template <class U, bool FLOAT, bool KV, int LT>
-__global__ void __launch_bounds__(BK_THREADS, 3) k_bucket_count(const U *keys, const uint32_t *vals, int64_t n,
+__global__ void __launch_bounds__(BK_THREADS, (BkShape<U, KV>::MINB)) k_bucket_count(const U *keys, const uint32_t *vals, int64_t n,
                                                              int64_t gidx_base, const U *sk, const uint32_t *sv,
                                                              const int64_t *sg, int ns, int64_t *cnt,
                                                              BucketGeom geom) {
     using B = Bucketer<U, FLOAT, KV>;
     constexpr bool SMALL = LT >= 0;  // <= 8 buckets: per-thread counts packed in registers
+    constexpr int BK_IPT = B::BK_IPT, BK_TILE = B::BK_TILE;
     __shared__ typename B::Split s;
     extern __shared__ __align__(16) unsigned char dyn[];
     uint32_t *hist = reinterpret_cast<uint32_t *>(dyn);  // [nb][BK_THREADS]: one column per thread
@@ -254,16 +265,19 @@ __global__ void __launch_bounds__(BK_SCAN_THREADS) k_bucket_scan(int64_t *cnt, i
 
 // Pass 3: stable scatter through a shared-memory staging tile grouped by bucket.
 // Staging slots are padded so that the 32 lanes of a warp, whose slots sit BK_IPT apart while a
-// bucket's run is filled, hit distinct banks: element slot p lives at p + p / 16, its bucket byte
-// at p + 4 * (p / 16).
-__device__ __forceinline__ int pad_w(int p) { return p + (p >> 4); }
-__device__ __forceinline__ int pad_b(int p) { return p + 4 * (p >> 4); }
+// bucket's run is filled, hit distinct banks: element slot p lives at p + p / BK_IPT, its bucket
+// byte at p + 4 (p / BK_IPT).
+template <int BK_IPT>
+__device__ __forceinline__ int pad_w(int p) { return p + p / BK_IPT; }
+template <int BK_IPT>
+__device__ __forceinline__ int pad_b(int p) { return p + 4 * (p / BK_IPT); }
 
 template <class U, bool KV>
 struct ScatterSmem {
-    U sk[BK_TILE + BK_TILE / 16];
-    uint32_t sv[KV ? BK_TILE + BK_TILE / 16 : 1];
-    uint8_t sb[BK_TILE + BK_TILE / 4];
+    static constexpr int BK_IPT = BkShape<U, KV>::IPT, BK_TILE = BkShape<U, KV>::TILE;
+    U sk[BK_TILE + BK_TILE / BK_IPT];
+    uint32_t sv[KV ? BK_TILE + BK_TILE / BK_IPT : 1];
+    uint8_t sb[BK_TILE + 4 * BK_TILE / BK_IPT];
     int32_t tstart[BK_MAX + 1];
     int64_t cur[BK_MAX];
     int64_t delta[BK_MAX];  // cur - tstart: global position of staging slot 0's bucket run
@@ -271,12 +285,13 @@ struct ScatterSmem {
 };
 
 template <class U, bool FLOAT, bool KV, int LT>
-__global__ void __launch_bounds__(BK_THREADS, 3) k_bucket_scatter(const U *keys, const uint32_t *vals, int64_t n,
+__global__ void __launch_bounds__(BK_THREADS, (BkShape<U, KV>::MINB)) k_bucket_scatter(const U *keys, const uint32_t *vals, int64_t n,
                                                                int64_t gidx_base, const U *sk, const uint32_t *sv,
                                                                const int64_t *sg, int ns, const int64_t *off,
                                                                U *out_keys, uint32_t *out_vals, BucketGeom geom) {
     using B = Bucketer<U, FLOAT, KV>;
     constexpr bool SMALL = LT >= 0;
+    constexpr int BK_IPT = B::BK_IPT, BK_TILE = B::BK_TILE;
     __shared__ typename B::Split s;
     extern __shared__ __align__(16) unsigned char dyn[];
     ScatterSmem<U, KV> &st = *reinterpret_cast<ScatterSmem<U, KV> *>(dyn);
@@ -345,17 +360,17 @@ __global__ void __launch_bounds__(BK_THREADS, 3) k_bucket_scatter(const U *keys,
                 } else {
                     p = (int)hist[b[j] * BK_THREADS + t]++;
                 }
-                st.sk[pad_w(p)] = k[j];
-                if (KV) st.sv[pad_w(p)] = v[j];
-                st.sb[pad_b(p)] = b[j];
+                st.sk[pad_w<BK_IPT>(p)] = k[j];
+                if (KV) st.sv[pad_w<BK_IPT>(p)] = v[j];
+                st.sb[pad_b<BK_IPT>(p)] = b[j];
             }
         }
         __syncthreads();
         const int tn = st.tstart[nb];
         for (int p = t; p < tn; p += BK_THREADS) {
-            const int64_t g = st.delta[st.sb[pad_b(p)]] + p;
-            out_keys[g] = st.sk[pad_w(p)];
-            if (KV) out_vals[g] = st.sv[pad_w(p)];
+            const int64_t g = st.delta[st.sb[pad_b<BK_IPT>(p)]] + p;
+            out_keys[g] = st.sk[pad_w<BK_IPT>(p)];
+            if (KV) out_vals[g] = st.sv[pad_w<BK_IPT>(p)];
         }
         if (t < nb) st.cur[t] += st.tstart[t + 1] - st.tstart[t];
     }

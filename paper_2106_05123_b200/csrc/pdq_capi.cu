@@ -324,7 +324,7 @@ extern "C" int pdq_sort_finish(void *workspace, pdq_stats *out, void *stream) {
 
 extern "C" size_t pdq_bucket_workspace_bytes(int64_t n, int nbuckets) {
     if (n < 0 || nbuckets < 1 || nbuckets > BK_MAX) return 0;
-    return a256((size_t)nbuckets * (size_t)bucket_geom(n).ctas * sizeof(int64_t));
+    return a256((size_t)nbuckets * (size_t)BK_MAX_CTAS * sizeof(int64_t));  // any element type's grid
 }
 
 namespace {
@@ -332,7 +332,7 @@ template <class U, bool FLOAT, bool KV, int LT>
 int launch_bucket(const void *keys, const uint32_t *vals, int64_t n, int64_t gidx_base, const void *sk,
                   const uint32_t *sv, const int64_t *sg, int ns, void *ok, uint32_t *ov, int64_t *bucket_counts,
                   int64_t *cnt, cudaStream_t s) {
-    const BucketGeom g = bucket_geom(n);
+    const BucketGeom g = bucket_geom(n, BkShape<U, KV>::TILE, BkShape<U, KV>::CTAS);
     const int nb = ns + 1;
     const size_t hist = (size_t)nb * BK_THREADS * sizeof(uint32_t);
     const size_t sc = sizeof(ScatterSmem<U, KV>) + hist;
