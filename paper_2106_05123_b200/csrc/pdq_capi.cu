@@ -390,6 +390,15 @@ extern "C" int pdq_bucket(const void *keys, int dtype, const uint32_t *payload, 
     }
     if (((uintptr_t)keys & 15) || ((uintptr_t)payload & 15))
         return set_err(PDQ_ERR_ALIGN, "keys and payload must be 16-byte aligned%s");
+    if (nsplit == 0) {  // one bucket: a copy
+        const int64_t cn = n;
+        cudaError_t e = cudaMemcpyAsync(out_keys, keys, (size_t)n * dtype_size(dtype), cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess && payload)
+            e = cudaMemcpyAsync(out_payload, payload, (size_t)n * 4, cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess)  // pageable source: staged before the call returns
+            e = cudaMemcpyAsync(bucket_counts, &cn, sizeof(cn), cudaMemcpyHostToDevice, s);
+        return e == cudaSuccess ? PDQ_OK : set_err(PDQ_ERR_CUDA, "bucket copy: %s", cudaGetErrorString(e));
+    }
     int64_t *cnt = (int64_t *)workspace;
     const bool kv = payload != nullptr;
 #define PDQ_BK(U, F) \
