@@ -140,7 +140,7 @@ def local_samples(keys, values, base: int, count: int):
             raw = raw & 0xFFFFFFFF
         smp[: pos.size, 0] = raw
         if values is not None:
-            smp[: pos.size, 1] = values[p].to(torch.int64) & 0xFFFFFFFF
+            smp[: pos.size, 1] = values.view(torch.int32)[p].to(torch.int64) & 0xFFFFFFFF
         smp[: pos.size, 2] = p + base
         smp[: pos.size, 3] = 1
     return smp
@@ -208,7 +208,8 @@ def sample_sort(keys, values=None, group=None, oversample: int = DEFAULT_OVERSAM
     out_v = None
     if values is not None:
         out_v = torch.empty(total, dtype=values.dtype, device=dev)
-        dist.all_to_all_single(out_v, bv, output_split_sizes=recv, input_split_sizes=send, group=group)
+        dist.all_to_all_single(out_v.view(torch.int32), bv.view(torch.int32), output_split_sizes=recv,
+                               input_split_sizes=send, group=group)  # payload bits as int32 (any backend)
 
     # 5. local sort of the received slice
     _local_sort(out_k, out_v, config)
