@@ -154,7 +154,7 @@ struct Bucketer {
             constexpr int PER = 16 / sizeof(U);
 #pragma unroll
             for (int j = 0; j < BK_IPT; j += PER) {
-                uint4 x = __ldcg((const uint4 *)(keys + e0 + j));
+                uint4 x = __ldg((const uint4 *)(keys + e0 + j));
                 if (sizeof(U) == 4) {
                     k[j] = (U)x.x, k[j + 1] = (U)x.y, k[j + 2] = (U)x.z, k[j + 3] = (U)x.w;
                 } else {
@@ -164,7 +164,7 @@ struct Bucketer {
             if (KV) {
 #pragma unroll
                 for (int j = 0; j < BK_IPT; j += 4) {
-                    uint4 y = __ldcg((const uint4 *)(vals + e0 + j));
+                    uint4 y = __ldg((const uint4 *)(vals + e0 + j));
                     v[j] = y.x, v[j + 1] = y.y, v[j + 2] = y.z, v[j + 3] = y.w;
                 }
             }
@@ -172,8 +172,8 @@ struct Bucketer {
 #pragma unroll
             for (int j = 0; j < BK_IPT; ++j) {
                 const bool in = e0 + j < hi;
-                k[j] = in ? ldcg(keys + e0 + j) : (U)0;
-                v[j] = (KV && in) ? ldcg(vals + e0 + j) : 0u;
+                k[j] = in ? __ldg(keys + e0 + j) : (U)0;
+                v[j] = (KV && in) ? __ldg(vals + e0 + j) : 0u;
             }
         }
     }
