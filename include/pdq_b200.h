@@ -137,8 +137,7 @@ size_t pdq_bucket_workspace_bytes(int64_t n, int nbuckets);
  * payload); element i goes to bucket b = number of splitters below (key_i, payload_i,
  * gidx_base + i), keys compared in the sort's order.  out_keys / out_payload (device, n elements)
  * (must not overlap the inputs) receive the elements grouped by bucket, stable within a bucket;
- * bucket_counts (device,
- * int64[nbuckets]) each bucket's size.  Asynchronous on `stream`. */
+ * bucket_counts (device, int64[nbuckets]) each bucket's size.  Asynchronous on `stream`. */
 int pdq_bucket(const void *keys, int dtype, const uint32_t *payload, int64_t n, int64_t gidx_base,
                const void *split_keys, const uint32_t *split_payload, const int64_t *split_gidx,
                int nsplit, void *out_keys, uint32_t *out_payload, int64_t *bucket_counts,
