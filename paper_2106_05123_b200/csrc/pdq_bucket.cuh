@@ -26,7 +26,7 @@ namespace pdq {
 
 constexpr int BK_THREADS = 256;
 constexpr int BK_MAX = 64;                       // buckets (ranks) per call
-constexpr int BK_MAX_CTAS = 148 * 8;             // upper bound of every element type's grid
+constexpr int BK_MAX_CTAS = 148 * 16;            // upper bound of every element type's grid
 
 // Per element type: elements per thread per tile (4-byte keys: 16, wider elements: 8, which keeps
 // them in registers without spilling) and the CTAs per SM the registers allow.
@@ -35,7 +35,11 @@ struct BkShape {
     static constexpr int IPT = (sizeof(U) == 4 && !KV) ? 16 : 8;
     static constexpr int TILE = BK_THREADS * IPT;
     static constexpr int MINB = IPT == 16 ? 3 : 4;
-    static constexpr int CTAS = 148 * 2 * MINB;
+#ifndef PDQ_BK_WAVES
+#define PDQ_BK_WAVES 4
+#endif
+    static constexpr int CTAS = 148 * PDQ_BK_WAVES * MINB;
+    static_assert(CTAS <= BK_MAX_CTAS, "the count workspace is sized for BK_MAX_CTAS CTAs");
 };
 constexpr int BK_SCAN_THREADS = 1024;
 
