@@ -1854,16 +1854,17 @@ struct WideLeaf {
                 rd[96 + warp] = vmx;
             }
             H::bsync();
-            kmn = (U)rd[0];
-            kmx = (U)rd[32];
-            vmn = (uint32_t)rd[64];
-            vmx = (uint32_t)rd[96];
-            for (int q = 1; q < 32; ++q) {
-                const U a = (U)rd[q], c = (U)rd[32 + q];
-                kmn = a < kmn ? a : kmn;
-                kmx = c > kmx ? c : kmx;
-                vmn = min(vmn, (uint32_t)rd[64 + q]);
-                vmx = max(vmx, (uint32_t)rd[96 + q]);
+            {  // lane q reads warp q's extremes; one warp reduction (every warp computes the same)
+                kmn = (U)rd[lane];
+                kmx = (U)rd[32 + lane];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const U a = shfl_x(kmn, o), c = shfl_x(kmx, o);
+                    kmn = a < kmn ? a : kmn;
+                    kmx = c > kmx ? c : kmx;
+                }
+                vmn = __reduce_min_sync(0xffffffffu, (uint32_t)rd[64 + lane]);
+                vmx = __reduce_max_sync(0xffffffffu, (uint32_t)rd[96 + lane]);
             }
             const U krange = kmx - kmn;
             if (krange == 0 && (!KV || vmn == vmx)) {
