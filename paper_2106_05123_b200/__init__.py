@@ -11,8 +11,10 @@ from .driver import (
     DEFAULT_CONFIG,
     MIN_BREAK_SIZE,
     DeviceSorter,
+    FieldOrder,
     HostPipeline,
     SortConfig,
+    by_field,
     is_bad_partition,
     sort,
     sort_device,
@@ -25,9 +27,11 @@ __version__ = "0.1.0"
 __all__ = [
     "DEFAULT_CONFIG",
     "DeviceSorter",
+    "FieldOrder",
     "HostPipeline",
     "MIN_BREAK_SIZE",
     "SortConfig",
+    "by_field",
     "is_bad_partition",
     "sort",
     "sort_device",

@@ -413,6 +413,67 @@ def _reverse_in_place(data) -> None:
         data.reverse()
 
 
+class FieldOrder:
+    """A fixed ordering of records by one field: ``lt(a, b)`` is
+    ``a[field] < b[field]`` (``>`` when descending).
+
+    It is an ordinary callable, the same shape as the reference's lambda orderings
+    (``sort_with(pairs, lambda a, b: a[0] < b[0])``, test_driver.py:198-204), so one object works
+    with both packages; ``sort_with`` / ``sort_with_config`` here recognise it and sort on the
+    device: the field's values are the keys, each record's index the payload, and the records are
+    permuted by the sorted indices.  Records with equal fields keep their input order (reversed
+    when descending) -- a valid result of the reference's unstable sort.  ``field`` is a position
+    (tuples, lists) or a name (numpy structured arrays)."""
+
+    def __init__(self, field=0, descending: bool = False):
+        self.field = field
+        self.descending = bool(descending)
+
+    def __call__(self, a, b) -> bool:
+        return a[self.field] > b[self.field] if self.descending else a[self.field] < b[self.field]
+
+    def __repr__(self) -> str:
+        return f"by_field({self.field!r}, descending={self.descending})"
+
+
+def by_field(field=0, descending: bool = False) -> FieldOrder:
+    """Ordering of records by ``record[field]`` (see FieldOrder)."""
+    return FieldOrder(field, descending)
+
+
+def _field_keys(col) -> np.ndarray:
+    kinds = {type(x) for x in col}
+    if kinds <= {int, bool}:
+        return _ints_to_int64(np.array(col, dtype=object))
+    if kinds <= {float, int}:
+        if any(type(x) is int and float(x) != x for x in col):
+            raise TypeError("mixed int/float field with ints not exactly representable as float64")
+        return np.array(col, dtype=np.float64)
+    raise TypeError(f"unsupported field types {sorted(k.__name__ for k in kinds)}")
+
+
+def _sort_records(data, order: FieldOrder, config: SortConfig) -> None:
+    n = len(data)
+    if n < 2:
+        return
+    if n > 0xFFFFFFFF:
+        raise ValueError("record sorts carry a uint32 index: at most 2^32 records")
+    if isinstance(data, np.ndarray) and data.dtype.names:
+        keys = np.ascontiguousarray(data[order.field])
+        if keys.dtype not in (np.int32, np.int64, np.float32, np.float64):
+            keys = keys.astype(np.float64 if keys.dtype.kind == "f" else np.int64)
+        keys = keys.copy()
+    else:
+        keys = _field_keys([rec[order.field] for rec in data])
+    idx = np.arange(n, dtype=np.uint32)
+    _sort_numpy(keys, idx, config)
+    perm = idx[::-1] if order.descending else idx
+    if isinstance(data, np.ndarray):
+        data[...] = data[perm]
+    else:
+        data[:] = [data[i] for i in perm.tolist()]
+
+
 def sort_with_config(data: MutableSequence, lt: Ordering, config: SortConfig,
                      branch_cheap: Optional[bool] = None) -> None:
     """Sort ``data`` in place under ``lt`` with explicit tunables (driver.py:282-292).
@@ -427,6 +488,9 @@ def sort_with_config(data: MutableSequence, lt: Ordering, config: SortConfig,
         _sort_any(data, config)
         _reverse_in_place(data)
         return
+    if isinstance(lt, FieldOrder):
+        _sort_records(data, lt, config)
+        return
     raise NotImplementedError(
-        "the B200 sort path implements the built-in orderings (operator.lt, operator.gt) only; "
+        "the B200 sort path implements the built-in orderings (operator.lt, operator.gt, by_field) only; "
         "custom Python orderings have no device equivalent and there is no CPU fallback")

@@ -138,3 +138,16 @@ def test_workload_generators_are_deterministic():
     assert not np.isnan(x).any() and not np.any((x == 0) & np.signbit(x))
     for k_ in workloads.C3_KS[:4]:
         assert np.unique(workloads.c3(k_, 1 << 16)).size <= k_
+
+
+def test_field_ordering_is_a_plain_comparator():
+    # by_field(i) works as the reference's lambda orderings do (test_driver.py:198-204)
+    from paper_2106_05123_b200 import by_field
+
+    lt = by_field(0)
+    assert lt((1, "b"), (2, "a")) and not lt((2, "a"), (1, "b")) and not lt((1, "x"), (1, "y"))
+    gt = by_field(1, descending=True)
+    assert gt((0, 5), (0, 3)) and not gt((0, 3), (0, 5))
+    assert by_field("w")({"w": 1.0}, {"w": 2.0})
+    with pytest.raises(RuntimeError):  # the device path is the only path
+        sort_with_config([(2, 0), (1, 1)], lt, DEFAULT_CONFIG)

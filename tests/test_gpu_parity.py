@@ -417,3 +417,40 @@ def test_sort_with_descending_ordering():
     ref = np.sort(t.cpu().numpy())[::-1]
     sort_with(t, operator.gt)
     assert same_bytes(t.cpu().numpy(), ref.copy())
+
+
+def test_sort_with_field_ordering():
+    # f4: key-field of a packed record.  The reference's test_custom_ordering (test_driver.py:198-204)
+    # sorts (key, index) tuples with `lambda a, b: a[0] < b[0]`; by_field(0) is that ordering as an
+    # object the device path recognises.  Same checks as the reference's test, plus the exact result
+    # (ties keep input order) and descending / structured-array / float variants.
+    import random
+    from collections import Counter
+
+    from paper_2106_05123_b200 import DEFAULT_CONFIG, by_field, sort_with_config
+
+    rng = random.Random(13)
+    arr = [(rng.randint(0, 9), i) for i in range(1000)]
+    work = list(arr)
+    sort_with(work, by_field(0))
+    assert [x[0] for x in work] == sorted(x[0] for x in arr)
+    assert Counter(work) == Counter(arr)
+    assert work == sorted(arr, key=lambda r: r[0])  # Python's sort is stable: ties in input order
+    work = list(arr)
+    sort_with(work, by_field(0, descending=True))
+    assert [x[0] for x in work] == sorted((x[0] for x in arr), reverse=True)
+    assert Counter(work) == Counter(arr)
+    recs = [(rng.random(), "r%d" % i, -i) for i in range(30001)]
+    work = list(recs)
+    sort_with_config(work, by_field(2), DEFAULT_CONFIG)
+    assert work == sorted(recs, key=lambda r: r[2])
+    work = list(recs)
+    sort_with(work, by_field(0))
+    assert work == sorted(recs, key=lambda r: r[0])
+    sa = np.zeros(50001, dtype=[("id", np.int32), ("w", np.float32)])
+    g = np.random.default_rng(4)
+    sa["id"] = np.arange(50001)
+    sa["w"] = g.standard_normal(50001).astype(np.float32)
+    want = sa[np.argsort(sa["w"], kind="stable")]
+    sort_with(sa, by_field("w"))
+    assert np.array_equal(sa, want)
