@@ -351,11 +351,14 @@ def _sort_any(data, config: SortConfig, values=None):
             stats = _sort_numpy(keys, vals, config)
             data[:] = list(zip(keys.tolist(), vals.tolist()))
             return stats
-        kinds = {type(x) for x in data}
+        kinds = set(map(type, data))
         if kinds <= {int}:
-            keys = _ints_to_int64(np.array(data, dtype=object))
+            try:
+                keys = np.fromiter(data, dtype=np.int64, count=n)
+            except OverflowError:
+                raise TypeError("integer keys must fit in int64") from None
         elif kinds <= {float}:
-            keys = np.array(data, dtype=np.float64)
+            keys = np.fromiter(data, dtype=np.float64, count=n)
         elif kinds <= {int, float}:
             keys = np.array(data, dtype=np.float64)
             if any(type(x) is int and float(x) != x for x in data):

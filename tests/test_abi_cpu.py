@@ -151,3 +151,12 @@ def test_field_ordering_is_a_plain_comparator():
     assert by_field("w")({"w": 1.0}, {"w": 2.0})
     with pytest.raises(RuntimeError):  # the device path is the only path
         sort_with_config([(2, 0), (1, 1)], lt, DEFAULT_CONFIG)
+
+
+def test_list_keys_outside_int64_are_rejected():
+    from paper_2106_05123_b200 import sort
+
+    with pytest.raises(TypeError):
+        sort([2**70, 1])
+    with pytest.raises(TypeError):
+        sort([1, "a"])
