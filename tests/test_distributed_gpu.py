@@ -11,7 +11,7 @@ import torch
 
 from paper_2106_05123_b200 import distributed as D
 from paper_2106_05123_b200 import sort_device
-from test_distributed_cpu import np_bucket, np_local_sort
+from test_distributed_cpu import np_bucket
 
 pytestmark = pytest.mark.gpu
 

@@ -5,7 +5,6 @@ Algorithmic bytes = 3 (w+p) n: the count pass reads the shard, the scatter pass 
 """
 import sys
 
-import numpy as np
 import torch
 
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
