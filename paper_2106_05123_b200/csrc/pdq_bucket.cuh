@@ -34,7 +34,10 @@ template <class U, bool KV>
 struct BkShape {
     static constexpr int IPT = (sizeof(U) == 4 && !KV) ? 16 : 8;
     static constexpr int TILE = BK_THREADS * IPT;
-    static constexpr int MINB = IPT == 16 ? 3 : 4;
+#ifndef PDQ_BK_MINB16
+#define PDQ_BK_MINB16 3
+#endif
+    static constexpr int MINB = IPT == 16 ? PDQ_BK_MINB16 : 4;
 #ifndef PDQ_BK_WAVES
 #define PDQ_BK_WAVES 4
 #endif
@@ -286,6 +289,7 @@ struct ScatterSmem {
     int64_t cur[BK_MAX];
     int64_t delta[BK_MAX];  // cur - tstart: global position of staging slot 0's bucket run
     int64_t part[BK_THREADS / 32];
+    uint64_t wp[2][2][BK_THREADS / 32];  // <= 8 buckets: per-warp 16-bit-field count totals, by tile parity
 };
 
 template <class U, bool FLOAT, bool KV, int LT>
@@ -306,7 +310,8 @@ __global__ void __launch_bounds__(BK_THREADS, (BkShape<U, KV>::MINB)) k_bucket_s
     __syncthreads();  // splitter table ready
     const int64_t lo = (int64_t)blockIdx.x * geom.per_cta;
     const int64_t hi = lo + geom.per_cta < n ? lo + geom.per_cta : n;
-    for (int64_t t0 = lo; t0 < hi; t0 += BK_TILE) {
+    int par = 0;
+    for (int64_t t0 = lo; t0 < hi; t0 += BK_TILE, par ^= 1) {
         U k[BK_IPT];
         uint32_t v[BK_IPT];
         uint8_t b[BK_IPT];
@@ -314,14 +319,65 @@ __global__ void __launch_bounds__(BK_THREADS, (BkShape<U, KV>::MINB)) k_bucket_s
         const int64_t e0 = t0 + (int64_t)t * BK_IPT;
         const int valid = hi - e0 >= BK_IPT ? BK_IPT : (hi > e0 ? (int)(hi - e0) : 0);
         B::template buckets<LT>(s, L, k, v, gidx_base + e0, valid, b);
-        uint64_t pk = 0;
-        if (SMALL) pk = B::packed_counts(b);
-        __syncthreads();  // the previous tile's readers of st / hist are done
-        if (SMALL) {
+        // (4-byte keys with <= 4 buckets keep the per-thread column pass below: cheaper at that size)
+        if constexpr (SMALL && (LT == 3 || BK_IPT == 8)) {
+            // Counts as 16-bit fields (buckets 0-3 in c0, 4-7 in c1; a tile holds <= 4096 elements), one
+            // warp scan of the packed words, per-warp totals through shared memory (double-buffered by
+            // tile parity), field-wise prefix sums by multiplication: no per-bucket shared-memory pass.
+            uint64_t c0 = 0, c1 = 0;
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (q < nb) hist[q * BK_THREADS + t] = (uint32_t)(pk >> (8 * q)) & 0xFFu;
-        } else {
+            for (int j = 0; j < BK_IPT; ++j) {
+                const uint64_t one = 1ull << (16 * (b[j] & 3));
+                if (b[j] < 4) c0 += one;
+                else if (b[j] != 0xFF) c1 += one;
+            }
+            uint64_t i0 = c0, i1 = c1;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint64_t y0 = __shfl_up_sync(0xffffffffu, i0, d), y1 = __shfl_up_sync(0xffffffffu, i1, d);
+                if (lane >= d) i0 += y0, i1 += y1;
+            }
+            if (lane == 31) st.wp[par][0][warp] = i0, st.wp[par][1][warp] = i1;
+            __syncthreads();  // (also: the previous tile's output loop is done with st.sk / sb / delta)
+            uint64_t w0 = 0, w1 = 0, T0 = 0, T1 = 0;
+#pragma unroll
+            for (int w = 0; w < BK_THREADS / 32; ++w) {
+                const uint64_t a = st.wp[par][0][w], a1 = st.wp[par][1][w];
+                if (w < warp) w0 += a, w1 += a1;
+                T0 += a, T1 += a1;
+            }
+            constexpr uint64_t M = 0x0001000100010001ull;  // field k of x * M = sum of fields 0..k of x
+            const uint64_t s0 = T0 * M - T0, s1 = T1 * M - T1 + ((T0 * M) >> 48) * M;  // tile bucket starts
+            uint64_t base0 = s0 + w0 + i0 - c0, base1 = s1 + w1 + i1 - c1;  // this thread's first slots
+            if (t < nb) {
+                const int f = 16 * (t & 3);
+                st.delta[t] = st.cur[t] - (int64_t)(((t < 4 ? s0 : s1) >> f) & 0xFFFFu);
+                st.cur[t] += (int64_t)(((t < 4 ? T0 : T1) >> f) & 0xFFFFu);
+            }
+#pragma unroll
+            for (int j = 0; j < BK_IPT; ++j) {
+                if (b[j] != 0xFF) {
+                    const int f = 16 * (b[j] & 3);
+                    const bool lo4 = b[j] < 4;
+                    const int p = (int)(((lo4 ? base0 : base1) >> f) & 0xFFFFu);
+                    if (lo4) base0 += 1ull << f;
+                    else base1 += 1ull << f;
+                    st.sk[pad_w<BK_IPT>(p)] = k[j];
+                    if (KV) st.sv[pad_w<BK_IPT>(p)] = v[j];
+                    st.sb[pad_b<BK_IPT>(p)] = b[j];
+                }
+            }
+            __syncthreads();
+            const int tn = (int)(hi - t0 < BK_TILE ? hi - t0 : BK_TILE);
+            for (int p = t; p < tn; p += BK_THREADS) {
+                const int64_t g = st.delta[st.sb[pad_b<BK_IPT>(p)]] + p;
+                out_keys[g] = st.sk[pad_w<BK_IPT>(p)];
+                if (KV) out_vals[g] = st.sv[pad_w<BK_IPT>(p)];
+            }
+            continue;
+        }
+        __syncthreads();  // the previous tile's readers of st / hist are done
+        {
             for (int q = 0; q < nb; ++q) hist[q * BK_THREADS + t] = 0;
 #pragma unroll
             for (int j = 0; j < BK_IPT; ++j)
