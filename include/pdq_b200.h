@@ -120,6 +120,13 @@ int pdq_sort_ex(void *keys, int dtype, uint32_t *payload, int64_t n, const pdq_c
                 void *workspace, size_t workspace_bytes, void *stream, void *event_sort_begin,
                 void *event_sort_end);
 
+/* pdq_sort() recording up to four caller-owned CUDA events (events[i] may be NULL, or events itself)
+ * on `stream` at the kernel boundaries of one sort: [0] before the first operation (state memsets,
+ * K4 check, init), [1] before the persistent partition kernel, [2] after it, [3] after the base-case
+ * kernel (the end of the sort).  For per-kernel timing without a profiler (bench.py). */
+int pdq_sort_timed(void *keys, int dtype, uint32_t *payload, int64_t n, const pdq_config *cfg,
+                   void *workspace, size_t workspace_bytes, void *stream, void *const *events);
+
 /* Synchronise `stream`, copy the device counters of the last sort that used
  * `workspace` into *stats (may be NULL) and return its status. */
 int pdq_sort_finish(void *workspace, pdq_stats *stats, void *stream);
@@ -142,6 +149,30 @@ int pdq_bucket(const void *keys, int dtype, const uint32_t *payload, int64_t n, 
                const void *split_keys, const uint32_t *split_payload, const int64_t *split_gidx,
                int nsplit, void *out_keys, uint32_t *out_payload, int64_t *bucket_counts,
                void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---- host-buffer drop-in (the reference's sort() on a host sequence, driver.py:267-270) ----
+ * The reference mutates the caller's host sequence in place.  A pdq_host_sorter owns device
+ * buffers (grown on demand), pinned staging slots and a pool of host threads; pdq_host_sort()
+ * copies the caller's keys (+ payload) to the device through the staging slots (T threads copy
+ * into pinned memory while the DMA of earlier slots runs), sorts them with pdq_sort_ex() and
+ * copies the result back into the same host buffers before it returns.  Synchronous; calls on one
+ * sorter are serialised; distinct sorters are independent. */
+typedef struct pdq_host_sorter pdq_host_sorter;
+
+/* threads <= 0: $PDQ_HOST_THREADS, else min(8, hardware threads).  NULL on failure. */
+pdq_host_sorter *pdq_host_sorter_create(int device, int threads);
+void pdq_host_sorter_destroy(pdq_host_sorter *h);
+
+/* keys / payload: HOST pointers (any alignment; payload may be NULL).  stats (may be NULL) receives
+ * the device counters.  phase_ms (may be NULL, 4 doubles): host ms staging+H2D, host ms sort wait,
+ * host ms D2H+copy-out, device ms of the sort alone.  Returns 0 or a negative pdq_status; on error
+ * the caller's buffers hold their input unless the failure was in the copy back. */
+int pdq_host_sort(pdq_host_sorter *h, void *keys, int dtype, uint32_t *payload, int64_t n, const pdq_config *cfg,
+                  pdq_stats *stats, double *phase_ms);
+
+/* Message for the last error of this sorter (CUDA failures; config/argument errors also set
+ * pdq_last_error() of the calling thread). */
+const char *pdq_host_sorter_error(const pdq_host_sorter *h);
 
 /* Thread-local message for the last error returned on this thread. */
 const char *pdq_last_error(void);

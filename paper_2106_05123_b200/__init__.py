@@ -13,8 +13,10 @@ from .driver import (
     DeviceSorter,
     FieldOrder,
     HostPipeline,
+    HostSorter,
     SortConfig,
     by_field,
+    host_sorter,
     is_bad_partition,
     sort,
     sort_device,
@@ -29,9 +31,11 @@ __all__ = [
     "DeviceSorter",
     "FieldOrder",
     "HostPipeline",
+    "HostSorter",
     "MIN_BREAK_SIZE",
     "SortConfig",
     "by_field",
+    "host_sorter",
     "is_bad_partition",
     "sort",
     "sort_device",

@@ -36,11 +36,16 @@ EXPORTS = (
     "pdq_workspace_bytes",
     "pdq_sort",
     "pdq_sort_ex",
+    "pdq_sort_timed",
     "pdq_sort_finish",
     "pdq_last_error",
     "pdq_version",
     "pdq_bucket_workspace_bytes",
     "pdq_bucket",
+    "pdq_host_sorter_create",
+    "pdq_host_sorter_destroy",
+    "pdq_host_sort",
+    "pdq_host_sorter_error",
 )
 
 
@@ -110,7 +115,8 @@ def build(verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     if not os.path.exists(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
         nvcc = "/usr/local/cuda/bin/nvcc"
-    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-o", LIB_PATH, os.path.join(CSRC, "pdq_capi.cu")]
+    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-o", LIB_PATH, os.path.join(CSRC, "pdq_capi.cu"),
+           os.path.join(CSRC, "pdq_host.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)
@@ -140,12 +146,23 @@ def lib() -> ctypes.CDLL:
             L.pdq_sort.restype = I
             L.pdq_sort_ex.argtypes = [P, I, P, I64, ctypes.POINTER(PdqConfig), P, SZ, P, P, P]
             L.pdq_sort_ex.restype = I
+            L.pdq_sort_timed.argtypes = [P, I, P, I64, ctypes.POINTER(PdqConfig), P, SZ, P, ctypes.POINTER(P)]
+            L.pdq_sort_timed.restype = I
             L.pdq_sort_finish.argtypes = [P, ctypes.POINTER(PdqStats), P]
             L.pdq_sort_finish.restype = I
             L.pdq_bucket_workspace_bytes.argtypes = [I64, I]
             L.pdq_bucket_workspace_bytes.restype = SZ
             L.pdq_bucket.argtypes = [P, I, P, I64, I64, P, P, P, I, P, P, P, P, SZ, P]
             L.pdq_bucket.restype = I
+            L.pdq_host_sorter_create.argtypes = [I, I]
+            L.pdq_host_sorter_create.restype = P
+            L.pdq_host_sorter_destroy.argtypes = [P]
+            L.pdq_host_sorter_destroy.restype = None
+            L.pdq_host_sort.argtypes = [P, P, I, P, I64, ctypes.POINTER(PdqConfig), ctypes.POINTER(PdqStats),
+                                        ctypes.POINTER(ctypes.c_double)]
+            L.pdq_host_sort.restype = I
+            L.pdq_host_sorter_error.argtypes = [P]
+            L.pdq_host_sorter_error.restype = ctypes.c_char_p
             L.pdq_last_error.argtypes = []
             L.pdq_last_error.restype = ctypes.c_char_p
             L.pdq_version.argtypes = []

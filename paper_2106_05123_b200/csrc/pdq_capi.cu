@@ -170,7 +170,7 @@ cudaError_t prepare(LaunchInfo &li) {
 }
 
 template <class U, bool FLOAT, bool KV>
-int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEvent_t ev1) {
+int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEvent_t ev1, cudaEvent_t ev_end) {
     LaunchInfo li;
     // (k_base_big reads a leaf as 16-byte vectors from its aligned base: up to 3 slots of lead-in)
     const int base_max = big_leaves<U, KV>() ? BIG_BASE - 4 : WideLeaf<U, FLOAT, KV>::CAP - 4;
@@ -200,6 +200,7 @@ int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEven
         k_base_big<FLOAT><<<(unsigned)(li.sms * li.occ_base), BigLeaf<FLOAT>::BT, BigLeaf<FLOAT>::bytes(), s>>>(P);
     else
         k_base_wide<U, FLOAT, KV><<<(unsigned)li.sms, 1024, WideLeaf<U, FLOAT, KV>::bytes(), s>>>(P);
+    if (ev_end) cudaEventRecord(ev_end, s);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "launch: %s", cudaGetErrorString(e));
     return PDQ_OK;
@@ -219,7 +220,14 @@ extern "C" int pdq_sort(void *keys, int dtype, uint32_t *payload, int64_t n, con
 
 extern "C" int pdq_sort_ex(void *keys, int dtype, uint32_t *payload, int64_t n, const pdq_config *cfg_in,
                            void *workspace, size_t ws_bytes, void *stream, void *ev_begin, void *ev_end) {
-    cudaEvent_t ev0 = (cudaEvent_t)ev_begin, ev1 = (cudaEvent_t)ev_end;
+    void *ev[4] = {nullptr, ev_begin, ev_end, nullptr};
+    return pdq_sort_timed(keys, dtype, payload, n, cfg_in, workspace, ws_bytes, stream, ev);
+}
+
+extern "C" int pdq_sort_timed(void *keys, int dtype, uint32_t *payload, int64_t n, const pdq_config *cfg_in,
+                              void *workspace, size_t ws_bytes, void *stream, void *const *events) {
+    cudaEvent_t evs = events ? (cudaEvent_t)events[0] : nullptr, ev0 = events ? (cudaEvent_t)events[1] : nullptr,
+                ev1 = events ? (cudaEvent_t)events[2] : nullptr, eve = events ? (cudaEvent_t)events[3] : nullptr;
     pdq_config cfg;
     if (cfg_in)
         cfg = *cfg_in;
@@ -238,12 +246,14 @@ extern "C" int pdq_sort_ex(void *keys, int dtype, uint32_t *payload, int64_t n, 
     if (((uintptr_t)workspace & 255)) return set_err(PDQ_ERR_ALIGN, "workspace must be 256-byte aligned%s");
     cudaStream_t s = (cudaStream_t)stream;
     unsigned char *ws = (unsigned char *)workspace;
+    if (evs) cudaEventRecord(evs, s);
     cudaError_t e = cudaMemsetAsync(ws + L.state, 0, sizeof(State), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(ws + L.ring, 0xFF, (size_t)(1ull << L.log_q) * 8, s);
     if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
     if (n == 0) {  // finish() reads a zeroed state: status 0
         if (ev0) cudaEventRecord(ev0, s);
         if (ev1) cudaEventRecord(ev1, s);
+        if (eve) cudaEventRecord(eve, s);
         return PDQ_OK;
     }
 
@@ -271,14 +281,14 @@ extern "C" int pdq_sort_ex(void *keys, int dtype, uint32_t *payload, int64_t n, 
 
     const bool kv = payload != nullptr;
 #ifdef PDQ_ONLY_I32  // profiling builds (tools/): int32 keys-only instantiation, fast to compile
-    if (dtype == PDQ_I32 && !kv) return launch<uint32_t, false, false>(P, s, L, ev0, ev1);
+    if (dtype == PDQ_I32 && !kv) return launch<uint32_t, false, false>(P, s, L, ev0, ev1, eve);
     return set_err(PDQ_ERR_DTYPE, "this profiling build sorts int32 keys only%s");
 #else
     switch (dtype) {
-        case PDQ_I32: return kv ? launch<uint32_t, false, true>(P, s, L, ev0, ev1) : launch<uint32_t, false, false>(P, s, L, ev0, ev1);
-        case PDQ_F32: return kv ? launch<uint32_t, true, true>(P, s, L, ev0, ev1) : launch<uint32_t, true, false>(P, s, L, ev0, ev1);
-        case PDQ_I64: return kv ? launch<uint64_t, false, true>(P, s, L, ev0, ev1) : launch<uint64_t, false, false>(P, s, L, ev0, ev1);
-        case PDQ_F64: return kv ? launch<uint64_t, true, true>(P, s, L, ev0, ev1) : launch<uint64_t, true, false>(P, s, L, ev0, ev1);
+        case PDQ_I32: return kv ? launch<uint32_t, false, true>(P, s, L, ev0, ev1, eve) : launch<uint32_t, false, false>(P, s, L, ev0, ev1, eve);
+        case PDQ_F32: return kv ? launch<uint32_t, true, true>(P, s, L, ev0, ev1, eve) : launch<uint32_t, true, false>(P, s, L, ev0, ev1, eve);
+        case PDQ_I64: return kv ? launch<uint64_t, false, true>(P, s, L, ev0, ev1, eve) : launch<uint64_t, false, false>(P, s, L, ev0, ev1, eve);
+        case PDQ_F64: return kv ? launch<uint64_t, true, true>(P, s, L, ev0, ev1, eve) : launch<uint64_t, true, false>(P, s, L, ev0, ev1, eve);
     }
 #endif
     return set_err(PDQ_ERR_DTYPE, "unsupported dtype code%s");

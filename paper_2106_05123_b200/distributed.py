@@ -61,18 +61,30 @@ def ordered_image(raw: np.ndarray, width: int, is_float: bool) -> np.ndarray:
     return u ^ sign
 
 
-def choose_splitters(samples: np.ndarray, nranks: int, width: int, is_float: bool) -> np.ndarray:
+def choose_splitters(samples: np.ndarray, nranks: int, width: int, is_float: bool,
+                     weights: Optional[np.ndarray] = None) -> np.ndarray:
     """P − 1 splitters from gathered samples: rows of (raw key bits, payload, global index).
 
-    Samples are ordered by (key in sort order, payload, global index) and the splitters are the
-    samples at positions ⌊k·M/P⌋, k = 1 .. P − 1 (M samples).  Every rank runs this on the same
-    gathered array, so every rank picks the same splitters."""
+    Samples are ordered by (key in sort order, payload, global index).  Each sample stands for
+    ``weights[i]`` elements of its shard (its shard's size over its shard's sample count), so a
+    short shard does not count as much as a long one; splitter k is the first sample at which the
+    cumulative weight reaches k/P of the total (unweighted: position ⌊k·M/P⌋).  Every rank runs this
+    on the same gathered array, so every rank picks the same splitters."""
     m = samples.shape[0]
     if nranks <= 1 or m == 0:
         return np.empty((0, 3), dtype=np.int64)
     ordk = ordered_image(samples[:, 0], width, is_float)
     order = np.lexsort((samples[:, 2], samples[:, 1], ordk))
-    picks = [(k * m) // nranks for k in range(1, nranks)]
+    if weights is None:
+        picks = [(k * m) // nranks for k in range(1, nranks)]
+    else:
+        cum = np.cumsum(np.asarray(weights, dtype=np.float64)[order])
+        tot = cum[-1]
+        # the last sample whose exclusive cumulative weight is <= k/P of the total (equal weights:
+        # floor(k M / P), the unweighted pick)
+        excl = cum - np.asarray(weights, dtype=np.float64)[order]
+        picks = [max(0, int(np.searchsorted(excl, k * tot / nranks * (1 + 1e-12), side="right")) - 1)
+                 for k in range(1, nranks)]
     return samples[order[picks]]
 
 
@@ -142,12 +154,23 @@ def local_samples(keys, values, base: int, count: int):
         if values is not None:
             smp[: pos.size, 1] = values.view(torch.int32)[p].to(torch.int64) & 0xFFFFFFFF
         smp[: pos.size, 2] = p + base
-        smp[: pos.size, 3] = 1
+        smp[: pos.size, 3] = n_local  # valid; the shard size weights this rank's samples
     return smp
 
 
 def valid_samples(rows: np.ndarray) -> np.ndarray:
-    return rows[rows[:, 3] == 1][:, :3]
+    return rows[rows[:, 3] > 0][:, :3]
+
+
+def sample_weights(rows: np.ndarray, per_rank: int) -> np.ndarray:
+    """Weight of each valid gathered sample: its shard's size over its shard's sample count."""
+    w = []
+    for r in range(rows.shape[0] // per_rank):
+        blk = rows[r * per_rank:(r + 1) * per_rank]
+        v = blk[blk[:, 3] > 0]
+        if v.shape[0]:
+            w.append(np.full(v.shape[0], float(v[0, 3]) / v.shape[0]))
+    return np.concatenate(w) if w else np.empty(0)
 
 
 # ---- the collective ----------------------------------------------------------------------------
@@ -188,8 +211,9 @@ def sample_sort(keys, values=None, group=None, oversample: int = DEFAULT_OVERSAM
     smp = local_samples(keys, values, base, S)
     allsmp = torch.empty((P * S, 4), dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(allsmp, smp, group=group)
-    g = valid_samples(allsmp.cpu().numpy())
-    splitters = choose_splitters(g, P, width, is_float)
+    rows = allsmp.cpu().numpy()
+    g = valid_samples(rows)
+    splitters = choose_splitters(g, P, width, is_float, sample_weights(rows, S))
     if splitters.shape[0] < P - 1:  # empty input everywhere: all buckets empty
         splitters = np.zeros((P - 1, 3), dtype=np.int64)
 

@@ -24,6 +24,7 @@ from __future__ import annotations
 import array
 import ctypes
 import operator
+import struct
 from dataclasses import dataclass
 from typing import Any, Callable, MutableSequence, Optional
 
@@ -151,7 +152,8 @@ class DeviceSorter:
 
     def run(self, keys, values=None, stream=None, events=None):
         """Enqueue the sort.  ``events=(begin, end)``: torch.cuda.Events (enable_timing)
-        recorded immediately around the persistent sorter kernel."""
+        recorded immediately around the persistent sorter kernel; four events: the kernel
+        boundaries of ``pdq_sort_timed`` (start, before / after the sorter, end of the sort)."""
         import torch
 
         if keys.numel() != self.n or _dtype_code(keys.dtype) != self.code:
@@ -159,14 +161,17 @@ class DeviceSorter:
         if (values is not None) != self.has_payload:
             raise TypeError("payload presence does not match this DeviceSorter")
         s = stream if stream is not None else torch.cuda.current_stream(keys.device)
-        ev = (None, None)
-        if events is not None:
-            ev = tuple(ctypes.c_void_p(e.cuda_event) for e in events)
-        rc = _lib.lib().pdq_sort_ex(
-            ctypes.c_void_p(keys.data_ptr()), self.code,
-            ctypes.c_void_p(values.data_ptr() if values is not None else 0), self.n,
-            ctypes.byref(self._cfg), ctypes.c_void_p(self.workspace.data_ptr()), self.nbytes,
-            ctypes.c_void_p(s.cuda_stream), ev[0], ev[1])
+        args = (ctypes.c_void_p(keys.data_ptr()), self.code,
+                ctypes.c_void_p(values.data_ptr() if values is not None else 0), self.n,
+                ctypes.byref(self._cfg), ctypes.c_void_p(self.workspace.data_ptr()), self.nbytes,
+                ctypes.c_void_p(s.cuda_stream))
+        with torch.cuda.device(self.workspace.device):  # the C side launches on the current device
+            if events is not None and len(events) == 4:
+                arr = (ctypes.c_void_p * 4)(*[e.cuda_event if e is not None else None for e in events])
+                rc = _lib.lib().pdq_sort_timed(*args, arr)
+            else:
+                ev = (None, None) if events is None else tuple(ctypes.c_void_p(e.cuda_event) for e in events)
+                rc = _lib.lib().pdq_sort_ex(*args, ev[0], ev[1])
         if rc != 0:
             _raise(rc, "pdq_sort")
 
@@ -175,8 +180,9 @@ class DeviceSorter:
 
         s = stream if stream is not None else torch.cuda.current_stream(self.workspace.device)
         st = _lib.PdqStats()
-        rc = _lib.lib().pdq_sort_finish(ctypes.c_void_p(self.workspace.data_ptr()), ctypes.byref(st),
-                                        ctypes.c_void_p(s.cuda_stream))
+        with torch.cuda.device(self.workspace.device):
+            rc = _lib.lib().pdq_sort_finish(ctypes.c_void_p(self.workspace.data_ptr()), ctypes.byref(st),
+                                            ctypes.c_void_p(s.cuda_stream))
         if rc != 0:
             _raise(rc, "pdq_sort_finish")
         return st.as_dict()
@@ -242,6 +248,12 @@ class HostPipeline:
 
         if len(inputs) != len(outputs):
             raise ValueError("inputs and outputs must pair up")
+        with torch.cuda.device(self.device):
+            return self._sort(inputs, outputs, events)
+
+    def _sort(self, inputs, outputs, events):
+        import torch
+
         ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
         h2d_done, sort_done, d2h_done = [], [], []
         if events is not None:
@@ -279,21 +291,88 @@ class HostPipeline:
 _ARRAY_CODES = {"i": np.int32, "l": np.int64, "q": np.int64, "f": np.float32, "d": np.float64}
 
 
-def _sort_numpy(keys: np.ndarray, values: Optional[np.ndarray], config: SortConfig):
+class HostSorter:
+    """The host-buffer drop-in of the C ABI (``pdq_host_sort``): sorts a host array in place the
+    way the reference's ``sort()`` mutates its sequence (driver.py:267-270).  One sorter owns device
+    buffers (grown on demand), pinned staging slots and a pool of host copy threads; the caller's
+    keys are staged into pinned memory by those threads while earlier chunks are in flight over
+    PCIe, sorted on the device, and copied back into the caller's buffer before ``sort`` returns."""
+
+    def __init__(self, device: int = 0, threads: int = 0):
+        self.device = int(device)
+        self._h = _lib.lib().pdq_host_sorter_create(self.device, int(threads))
+        if not self._h:
+            raise RuntimeError(f"pdq_host_sorter_create failed on device {self.device}: {_lib.last_error()}")
+
+    def sort(self, keys: np.ndarray, values: Optional[np.ndarray] = None, config: SortConfig = DEFAULT_CONFIG,
+             phases: bool = False):
+        """Sort the C-contiguous 1-D numpy array ``keys`` (int32/int64/float32/float64) in place, with
+        an optional uint32 ``values`` payload.  Returns the device counters (and, with
+        ``phases=True``, the (h2d, sort, d2h, device-sort) milliseconds)."""
+        code = _NP_CODE.get(keys.dtype)
+        if code is None:
+            raise TypeError(f"unsupported key dtype {keys.dtype}; expected int32, int64, float32 or float64")
+        if keys.ndim != 1 or not keys.flags.c_contiguous or not keys.flags.writeable:
+            raise TypeError("keys must be a writeable C-contiguous 1-D array")
+        if values is not None:
+            if values.dtype != np.uint32 or values.shape != keys.shape or not values.flags.c_contiguous:
+                raise TypeError("values must be a C-contiguous uint32 array of the keys' shape")
+        st = _lib.PdqStats()
+        ph = (ctypes.c_double * 4)()
+        cfg = config.to_c()
+        rc = _lib.lib().pdq_host_sort(
+            ctypes.c_void_p(self._h), ctypes.c_void_p(keys.ctypes.data), code,
+            ctypes.c_void_p(values.ctypes.data if values is not None else 0), int(keys.size), ctypes.byref(cfg),
+            ctypes.byref(st), ph)
+        if rc != 0:
+            if rc == -5:
+                raise RuntimeError(f"pdq_host_sort: {_lib.STATUS.get(rc, rc)}: "
+                                   f"{_lib.lib().pdq_host_sorter_error(ctypes.c_void_p(self._h)).decode()}")
+            _raise(rc, "pdq_host_sort")
+        stats = st.as_dict()
+        return (stats, tuple(ph)) if phases else stats
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.lib().pdq_host_sorter_destroy(ctypes.c_void_p(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_NP_CODE = {np.dtype(np.int32): _lib.PDQ_I32, np.dtype(np.int64): _lib.PDQ_I64,
+            np.dtype(np.float32): _lib.PDQ_F32, np.dtype(np.float64): _lib.PDQ_F64}
+_HOST_SORTERS = {}
+
+
+def host_sorter(device: Optional[int] = None) -> HostSorter:
+    """The process's cached :class:`HostSorter` for ``device`` (default: the current CUDA device)."""
     import torch
 
     if not torch.cuda.is_available():
         raise RuntimeError("no CUDA device: the B200 sort path has no CPU fallback")
-    kt = torch.from_numpy(np.ascontiguousarray(keys))
-    dev = torch.device("cuda")
-    kd = kt.to(dev, non_blocking=False)
-    vd = None
-    if values is not None:
-        vd = torch.from_numpy(np.ascontiguousarray(values).view(np.int32)).to(dev)
-    stats = sort_device(kd, vd, config)
-    keys[...] = kd.cpu().numpy()
-    if values is not None:
-        values[...] = vd.cpu().numpy().view(np.uint32)
+    d = torch.cuda.current_device() if device is None else int(device)
+    hs = _HOST_SORTERS.get(d)
+    if hs is None:
+        hs = _HOST_SORTERS[d] = HostSorter(d)
+    return hs
+
+
+def _sort_numpy(keys: np.ndarray, values: Optional[np.ndarray], config: SortConfig):
+    """Host array -> device -> sorted -> the same host array, through ``pdq_host_sort``."""
+    k = keys if keys.flags.c_contiguous and keys.flags.writeable else np.ascontiguousarray(keys).copy()
+    v = values
+    if values is not None and not values.flags.c_contiguous:
+        v = np.ascontiguousarray(values).copy()
+    stats = host_sorter().sort(k, v, config)
+    if k is not keys:
+        keys[...] = k
+    if v is not values:
+        values[...] = v
     return stats
 
 
@@ -343,11 +422,22 @@ def _sort_any(data, config: SortConfig, values=None):
             if values is not None:
                 raise TypeError("values= cannot be combined with (key, payload) tuples")
             if any(type(p) is not tuple or len(p) != 2 for p in data):
-                raise TypeError("tuple elements must all be (int key, uint32 payload) pairs")
-            ks = np.array([p[0] for p in data], dtype=object)
-            vs = np.array([p[1] for p in data], dtype=object)
-            keys = _ints_to_int64(ks)
-            vals = _as_payload(_ints_to_int64(vs))
+                raise TypeError("tuple elements must all be (key, uint32 payload) pairs")
+            kcol = [p[0] for p in data]
+            vcol = [p[1] for p in data]
+            # the element types are checked before any conversion: a float key is never truncated to
+            # an int, and nothing but an int is accepted as a payload
+            if any(type(v) is not int for v in vcol):
+                raise TypeError("tuple payloads must be ints in [0, 2^32)")
+            kkinds = set(map(type, kcol))
+            if kkinds <= {int}:
+                keys = _ints_to_int64(np.array(kcol, dtype=object))
+            elif kkinds <= {float}:
+                keys = np.array(kcol, dtype=np.float64)
+            else:
+                raise TypeError(f"tuple keys must be all ints or all floats, got "
+                                f"{sorted(k.__name__ for k in kkinds)}")
+            vals = _as_payload(_ints_to_int64(np.array(vcol, dtype=object)))
             stats = _sort_numpy(keys, vals, config)
             data[:] = list(zip(keys.tolist(), vals.tolist()))
             return stats
@@ -374,13 +464,22 @@ def _sort_any(data, config: SortConfig, values=None):
         out = keys.tolist()
         if kinds == {int, float}:
             # keep each element's original Python type (ints stay ints)
+            # keyed by the float64 bit pattern: NaN != NaN, but its bits match
             pool = {}
             for x in data:
-                pool.setdefault((float(x), type(x)), []).append(x)
-            out = [(pool[(v, int)].pop() if pool.get((v, int)) else pool[(v, float)].pop()) for v in out]
+                pool.setdefault((_f64_bits(x), type(x)), []).append(x)
+            res = []
+            for v in out:
+                kb = _f64_bits(v)
+                res.append(pool[(kb, int)].pop() if pool.get((kb, int)) else pool[(kb, float)].pop())
+            out = res
         data[:] = out
         return stats
     raise TypeError(f"unsupported container {type(data).__name__}")
+
+
+def _f64_bits(x) -> int:
+    return struct.unpack("<q", struct.pack("<d", float(x)))[0]
 
 
 def _ints_to_int64(objs: np.ndarray) -> np.ndarray:
@@ -463,6 +562,8 @@ def _sort_records(data, order: FieldOrder, config: SortConfig) -> None:
         raise ValueError("record sorts carry a uint32 index: at most 2^32 records")
     if isinstance(data, np.ndarray) and data.dtype.names:
         keys = np.ascontiguousarray(data[order.field])
+        if keys.dtype == np.uint64 and keys.size and int(keys.max()) >= 1 << 63:
+            raise TypeError("uint64 field values >= 2^63 do not fit the int64 key type")
         if keys.dtype not in (np.int32, np.int64, np.float32, np.float64):
             keys = keys.astype(np.float64 if keys.dtype.kind == "f" else np.int64)
         keys = keys.copy()

@@ -160,3 +160,32 @@ def test_list_keys_outside_int64_are_rejected():
         sort([2**70, 1])
     with pytest.raises(TypeError):
         sort([1, "a"])
+
+
+def test_tuple_elements_are_type_checked_before_conversion():
+    # float payloads / mixed keys in (key, payload) tuples must raise, never be
+    # truncated and written back
+    from paper_2106_05123_b200 import sort
+
+    cases = [
+        [(1, 0.5), (2, 1)],          # float payload
+        [(1, 2), (2.5, 1)],          # mixed int/float keys
+        [(1, "7"), (0, 1)],          # string payload
+        [("3", 1), (2, 0)],          # string key
+        [(1, -1), (0, 1)],           # negative payload
+    ]
+    for c in cases:
+        w = list(c)
+        with pytest.raises(TypeError):
+            sort(w)
+        assert w == c  # untouched
+
+
+def test_uint64_field_beyond_int64_is_rejected():
+    # a uint64 field value >= 2^63 would wrap negative as an int64 key
+    from paper_2106_05123_b200 import by_field, sort_with
+
+    rec = np.zeros(2, dtype=[("k", np.uint64), ("v", np.int32)])
+    rec["k"] = [2**63 + 1, 5]
+    with pytest.raises(TypeError):
+        sort_with(rec, by_field("k"))

@@ -69,7 +69,7 @@ def np_local_sort(keys, values, config):
 def make_case(name, world, rank):
     rng = np.random.default_rng(1000 + 17 * world)
     sizes = {"int32": [5000, 3000, 4000], "kv": [4000, 0, 2500], "float": [3000, 3001, 1],
-             "equal": [6000, 6000, 6000], "empty": [0, 0, 0]}[name][:world]
+             "equal": [6000, 6000, 6000], "empty": [0, 0, 0], "skewed": [20000, 300, 300]}[name][:world]
     parts = []
     for r in range(world):
         n = sizes[r]
@@ -88,6 +88,8 @@ def make_case(name, world, rank):
             parts.append((torch.from_numpy(x), None))
         elif name == "equal":
             parts.append((torch.full((n,), 7, dtype=torch.int64), None))
+        elif name == "skewed":  # very unequal shards over disjoint key ranges (weighting)
+            parts.append((torch.from_numpy(rng.integers(1000 * r, 1000 * r + 1000, n, dtype=np.int64)), None))
         else:
             parts.append((torch.empty(0, dtype=torch.int32), None))
     return parts
@@ -106,7 +108,7 @@ def _worker(rank, world, port, name, out):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("name", ["int32", "kv", "float", "equal", "empty"])
+@pytest.mark.parametrize("name", ["int32", "kv", "float", "equal", "empty", "skewed"])
 def test_sample_sort_gloo(world, name):
     mgr = mp.Manager()
     out = mgr.dict()
@@ -119,9 +121,10 @@ def test_sample_sort_gloo(world, name):
     assert got_k == _bits(keys).tolist()
     if vals is not None:
         assert sum((out[r][1] for r in range(world)), []) == vals.numpy().tolist()
-    if name == "equal":  # ties broken by global index: every rank gets about a third
+    if name in ("equal", "skewed"):  # ties by global index; samples weighted by shard size
+        tol = 0.1 if name == "equal" else 0.3  # skewed: 96 random samples of the big shard per rank
         for r in range(world):
-            assert abs(len(out[r][0]) - keys.numel() / world) < 0.1 * keys.numel() / world
+            assert abs(len(out[r][0]) - keys.numel() / world) < tol * keys.numel() / world
 
 
 def test_splitter_choice_is_rank_independent_and_ordered():
@@ -133,6 +136,24 @@ def test_splitter_choice_is_rank_independent_and_ordered():
     ok = D.ordered_image(a[:, 0], 4, False)
     assert (np.diff(ok.astype(np.float64)) >= 0).all()
     assert D.choose_splitters(s, 1, 4, False).shape == (0, 3)
+
+
+def test_weighted_splitters_follow_shard_sizes():
+    # rank 0: 10 samples standing for 10000 keys in [0, 100); rank 1: 10 samples for 10 keys in [100, 110)
+    s0 = np.stack([np.arange(0, 100, 10), np.zeros(10, np.int64), np.arange(10)], axis=1)
+    s1 = np.stack([np.arange(100, 110), np.zeros(10, np.int64), 10000 + np.arange(10)], axis=1)
+    s = np.concatenate([s0, s1])
+    w = np.concatenate([np.full(10, 1000.0), np.full(10, 1.0)])
+    unweighted = D.choose_splitters(s, 2, 8, False)
+    weighted = D.choose_splitters(s, 2, 8, False, w)
+    assert unweighted[0, 0] == 100            # half the samples: the small shard's range
+    assert 40 <= weighted[0, 0] <= 60         # half the weight: the middle of the big shard
+    eq = D.choose_splitters(s, 4, 8, False, np.ones(20))
+    assert (eq == D.choose_splitters(s, 4, 8, False)).all()  # equal weights = the unweighted picks
+    rows = np.zeros((8, 4), np.int64)
+    rows[:3, 3] = 300
+    rows[4:8, 3] = 40
+    assert list(D.sample_weights(rows, 4)) == [100.0] * 3 + [10.0] * 4
 
 
 def test_ordered_image_matches_numeric_order():
