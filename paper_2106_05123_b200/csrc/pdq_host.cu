@@ -28,7 +28,7 @@
 
 namespace {
 
-constexpr size_t CHUNK = 8u << 20;  // bytes per staging slot
+constexpr size_t CHUNK_DEFAULT = 8u << 20;  // bytes per staging slot ($PDQ_HOST_CHUNK_KB overrides)
 
 struct Seg1 {  // one array to transfer: host <-> device, `bytes` long
     unsigned char *host;
@@ -54,6 +54,7 @@ struct pdq_host_sorter {
     unsigned char *d_keys = nullptr, *d_vals = nullptr, *d_ws = nullptr;
     size_t cap_keys = 0, cap_vals = 0, cap_ws = 0;
     int nthreads = 1;
+    size_t chunk = CHUNK_DEFAULT;
     std::vector<Worker> w;
     // job dispatch to the worker pool
     std::mutex mu;
@@ -111,10 +112,10 @@ struct ChunkRef {
     const Seg1 *s;
     size_t off, bytes;
 };
-std::vector<ChunkRef> chunk_list(const std::vector<Seg1> &segs) {
+std::vector<ChunkRef> chunk_list(const std::vector<Seg1> &segs, size_t chunk) {
     std::vector<ChunkRef> out;
     for (const Seg1 &s : segs)
-        for (size_t off = 0; off < s.bytes; off += CHUNK) out.push_back({&s, off, std::min(CHUNK, s.bytes - off)});
+        for (size_t off = 0; off < s.bytes; off += chunk) out.push_back({&s, off, std::min(chunk, s.bytes - off)});
     return out;
 }
 
@@ -194,6 +195,10 @@ extern "C" pdq_host_sorter *pdq_host_sorter_create(int device, int threads) {
         }
     }
     h->nthreads = std::min(threads, 64);
+    if (const char *ck = getenv("PDQ_HOST_CHUNK_KB")) {
+        const long kb = atol(ck);
+        if (kb >= 64 && kb <= (256l << 10)) h->chunk = (size_t)kb << 10;
+    }
     bool ok = cudaSetDevice(device) == cudaSuccess && cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) == cudaSuccess;
     for (cudaEvent_t *e : {&h->ev_h2d, &h->ev_sort, &h->ev_k0, &h->ev_k1, &h->ev_t0})
         ok = ok && cudaEventCreate(e) == cudaSuccess;
@@ -201,7 +206,7 @@ extern "C" pdq_host_sorter *pdq_host_sorter_create(int device, int threads) {
     for (Worker &w : h->w) {
         ok = ok && cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking) == cudaSuccess;
         for (int k = 0; k < 2; ++k) {
-            ok = ok && cudaHostAlloc((void **)&w.slot[k], CHUNK, cudaHostAllocPortable) == cudaSuccess;
+            ok = ok && cudaHostAlloc((void **)&w.slot[k], h->chunk, cudaHostAllocPortable) == cudaSuccess;
             ok = ok && cudaEventCreateWithFlags(&w.ev[k], cudaEventDisableTiming) == cudaSuccess;
         }
         ok = ok && cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming) == cudaSuccess;
@@ -266,7 +271,7 @@ extern "C" int pdq_host_sort(pdq_host_sorter *h, void *keys, int dtype, uint32_t
 
     std::vector<Seg1> segs{{(unsigned char *)keys, h->d_keys, kb}};
     if (payload) segs.push_back({(unsigned char *)payload, h->d_vals, vb});
-    const std::vector<ChunkRef> ch = chunk_list(segs);
+    const std::vector<ChunkRef> ch = chunk_list(segs, h->chunk);
     for (Worker &wk : h->w) wk.rc = 0;
 
     // 1. H2D through the pinned slots (all workers)

@@ -22,6 +22,7 @@
 #pragma once
 
 #include "pdq_device.cuh"
+#include "pdq_networks.cuh"
 
 namespace pdq {
 
@@ -69,6 +70,8 @@ struct Shared {
     Seg nseg;
     unsigned long long npos; // ring position claimed for the next task
     uint64_t lf[2];          // K7: descriptors of the current and the next leaf
+    uint64_t lq[3];          // K7 (k_base_big): current, next and claimed-after-next leaf descriptors
+    long long lc0;           // K7: cycle stamp of the current leaf (counters)
     int nstate;              // 0 none, 1 claimed (unpublished), 2 ready, 3 exit
     // load cursor (thread 0): tiles issued so far, and which task/tile is the next to load
     unsigned li;             // loads issued (stage li % NST)
@@ -1445,40 +1448,172 @@ struct BigLeaf {
         }
     }
 
+    // ---- fast path: window networks over a swizzled kc ----------------------------------------------
+    // Positions are in q-space: q = a0 + leaf position, a0 = b mod 4, so q and the leaf's global index
+    // have the same 16-byte phase.  Row t = q / 24 is thread t's window; its six 16-byte chunks are
+    // rotated by one in rows with bit 2 of t set, so the 8 lanes of a quarter-warp reading their own
+    // rows (or the next rows) hit 8 distinct bank groups.
+    static constexpr int WIN = 24, HALF = WIN / 2;
+    static constexpr uint32_t FAST_CMAX = HALF + 1;  // every bucket fits an aligned or an offset window
+    static_assert(BIG_BASE == WIN * BT, "one window per thread");
+    __device__ __forceinline__ static uint32_t swz_chunk(uint32_t t, uint32_t j) {
+        uint32_t jj = j + ((t >> 2) & 1u);
+        jj = jj >= 6u ? jj - 6u : jj;
+        return WIN * t + 4u * jj;
+    }
+    __device__ __forceinline__ static uint32_t swz(uint32_t q) {
+        const uint32_t t = q / (uint32_t)WIN, r = q - (uint32_t)WIN * t;
+        return swz_chunk(t, r >> 2) + (r & 3u);
+    }
+    __device__ __forceinline__ static void ld_chunk(const uint32_t *s, U *w) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(s);
+        w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+    }
+    __device__ __forceinline__ static void st_chunk(uint32_t *s, const U *w) {
+        *reinterpret_cast<uint4 *>(s) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    // Sort the bucketed leaf kc[q], q in [a0, qend) (swizzled), and store it to dst[q - a0] (global):
+    //   pass 1: thread t sorts window [24t, 24t + 24) with a 132-comparator network;
+    //   pass 2: thread t merges the two sorted halves of the offset window [24t + 12, 24t + 36) (45
+    //           comparators) and writes it back to the same (swizzled) chunks it read -- windows are
+    //           disjoint, so no barrier separates its loads from its stores;
+    //   copy-out: consecutive threads read consecutive 16-byte chunks in linear order and store them to
+    //           global memory (raw keys), 512 contiguous bytes per warp instruction.
+    // Each element only moves inside its bucket; a bucket of <= 13 keys lies in one aligned or one offset
+    // window, so after the two passes every bucket -- and so the leaf -- is in order.  Slots q < a0 read
+    // as 0 (below every key), q >= qend as ~0 (above every key); neither is ever stored.
+    __device__ __forceinline__ static void window_sort(uint32_t *kc, uint32_t a0, uint32_t qend, U *dst) {
+        const uint32_t t = threadIdx.x;
+        if (WIN * t < qend) {
+            U w[WIN];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) ld_chunk(kc + swz_chunk(t, j), w + 4 * j);
+#pragma unroll
+            for (int i = 0; i < WIN; ++i) {
+                const uint32_t q = WIN * t + i;
+                w[i] = q < a0 ? 0u : (q >= qend ? ~0u : w[i]);
+            }
+            net_sort24(w);
+#pragma unroll
+            for (int j = 0; j < 6; ++j) st_chunk(kc + swz_chunk(t, j), w + 4 * j);
+        }
+        bsync();
+        if (WIN * t + HALF < qend) {
+            U w[WIN];
+            const bool second = WIN * (t + 1) < qend;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) ld_chunk(kc + swz_chunk(t, j + 3), w + 4 * j);
+            if (second) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) ld_chunk(kc + swz_chunk(t + 1, j), w + HALF + 4 * j);
+            } else {
+#pragma unroll
+                for (int i = HALF; i < WIN; ++i) w[i] = ~0u;
+            }
+#pragma unroll
+            for (int i = HALF; i < WIN; ++i) {
+                const uint32_t q = WIN * t + HALF + i;
+                w[i] = q >= qend ? ~0u : w[i];
+            }
+            net_merge12(w);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) st_chunk(kc + swz_chunk(t, j + 3), w + 4 * j);
+            if (second) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) st_chunk(kc + swz_chunk(t + 1, j), w + HALF + 4 * j);
+            }
+        }
+        bsync();
+        // copy-out: linear chunk c = q / 4; dst + (4c - a0) is 16-byte aligned
+        const uint32_t nch = (qend + 3) / 4;
+        for (uint32_t c = t; c < nch; c += BT) {
+            U v[4];
+            ld_chunk(kc + swz_chunk(c / 6u, c % 6u), v);
+            const uint32_t q = 4 * c;
+            if (q >= a0 && q + 4 <= qend) {
+                *reinterpret_cast<uint4 *>(dst + (q - a0)) = make_uint4(O::from(v[0]), O::from(v[1]), O::from(v[2]),
+                                                                        O::from(v[3]));
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (q + e >= a0 && q + e < qend) dst[q + e - a0] = O::from(v[e]);
+            }
+        }
+    }
+
+    // thread 0: TMA bulk load of leaf `lf` into kd (from its 16-byte aligned base; the array's last
+    // partial vector by scalar loads), completing on `bar`
+    __device__ __forceinline__ static void prefetch(const Params &P, uint64_t lf, uint32_t *kd, uint64_t *bar) {
+        const int m = (int)((lf >> 1) & 0x7FFF) + 1;
+        const int64_t b = (int64_t)(lf >> 16);
+        const int off = (int)(b & 3);
+        const int64_t base = b - off;
+        const U *src = (const U *)((lf & 1u) ? P.b_keys : P.a_keys) + base;
+        const int64_t vec = ((int64_t)(off + m) + 3) & ~(int64_t)3;
+        const int64_t room = P.n - base;
+        const int64_t bulk = vec < (room & ~(int64_t)3) ? vec : (room & ~(int64_t)3);
+        for (int64_t e = bulk; e < vec && e < room; ++e) kd[e] = ldcg(src + e);
+        fence_proxy_async();
+        mbar_expect_tx(bar, (unsigned)(bulk * 4));
+        if (bulk > 0) bulk_g2s(kd, src, (unsigned)(bulk * 4), bar);
+    }
+    // every thread: its registers of leaf `lf` from kd (the register layout of load())
+    __device__ __forceinline__ static void read_kd(const uint32_t *kd, uint64_t lf, U (&xs)[BI]) {
+        const int tid = threadIdx.x;
+        const int m = (int)((lf >> 1) & 0x7FFF) + 1;
+        const int off = (int)((lf >> 16) & 3);
+#pragma unroll
+        for (int jv = 0; jv < BI / 4; ++jv) {
+            const int e0 = 4 * (jv * BT + tid);
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (e0 < off + m) v = *reinterpret_cast<const uint4 *>(kd + e0);
+            xs[4 * jv] = v.x;
+            xs[4 * jv + 1] = v.y;
+            xs[4 * jv + 2] = v.z;
+            xs[4 * jv + 3] = v.w;
+        }
+    }
+
     __device__ static void run(const Params &P) {
+        // Per-leaf scalars that only thread 0 needs (descriptors ahead, counters) live in shared memory:
+        // with 1024 threads every register is precious (24 keys + 12 packed slots per thread).
         Shared &sh = g_sh;
         const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
         uint32_t *kc = wd(), *kd = wd() + KD_OFF, *cnt = wd() + CNT_OFF, *red = wd() + RED_OFF;
-        unsigned long long count = *(volatile unsigned long long *)&P.st->leaf_count;
-        if (count > P.leaf_cap) count = P.leaf_cap;
         constexpr uint64_t NONE = ~0ull;
-        auto claim = [&](int k) {
-            if (tid == 0) {
-                const unsigned long long idx = atomicAdd(&P.st->leaf_next, 1ull);
-                sh.lf[k] = idx < count ? ldcg(P.leaves + idx) : NONE;
-            }
+        uint64_t *bar = &sh.bar[0];
+        auto claim = [&]() -> uint64_t {  // thread 0
+            unsigned long long count = *(volatile unsigned long long *)&P.st->leaf_count;
+            if (count > P.leaf_cap) count = P.leaf_cap;
+            const unsigned long long idx = atomicAdd(&P.st->leaf_next, 1ull);
+            return idx < count ? ldcg(P.leaves + idx) : NONE;
         };
-        U xs[BI];
-        claim(0);
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            sh.lq[0] = claim();
+            sh.lq[1] = sh.lq[0] == NONE ? NONE : claim();
+            if (sh.lq[0] != NONE) prefetch(P, sh.lq[0], kd, bar);
+        }
         bsync();
-        uint64_t cur = sh.lf[0];
-        int k = 0;
-        load(P, cur, xs);
+        U xs[BI];
+        unsigned kphase = 0;
         long long pm = clock64();  // (PDQ_BIG_PHASES profiling builds)
-        while (cur != NONE) {
-            const long long c0 = clock64();
-            pm = c0;
-            // thread 0 claims the next leaf; its descriptor stays in a register until the barrier before
-            // the ranking phase, so the round trips never stall the barriers in between
-            uint64_t pend = NONE;
+        for (;;) {
+            const uint64_t cur = sh.lq[0];
+            if (cur == NONE) break;
             if (tid == 0) {
-                const unsigned long long idx = atomicAdd(&P.st->leaf_next, 1ull);
-                if (idx < count) pend = ldcg(P.leaves + idx);
+                sh.lc0 = clock64();
+                sh.lq[2] = sh.lq[1] != NONE ? claim() : NONE;  // its round trip overlaps this leaf
             }
+            pm = clock64();
+            mbar_wait(bar, kphase);
+            kphase ^= 1u;
+            read_kd(kd, cur, xs);
             const int m = (int)((cur >> 1) & 0x7FFF) + 1;
             const int64_t b = (int64_t)(cur >> 16);
             const bool srcB = cur & 1u;
-            {  // zero the bucket counters while the loads are in flight
+            {  // zero the bucket counters
                 uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
 #pragma unroll
                 for (int q = 0; q < BBK / 4 / BT; ++q) c4[q * BT + tid] = make_uint4(0, 0, 0, 0);
@@ -1500,7 +1635,8 @@ struct BigLeaf {
                 red[64 + warp] = mn;
                 red[96 + warp] = mx;
             }
-            bsync();
+            bsync();  // kd has been read by every thread: the next leaf's load may land in it
+            if (tid == 0 && sh.lq[1] != NONE) prefetch(P, sh.lq[1], kd, bar);
             PHASE_MARK(0);
             mn = __reduce_min_sync(0xffffffffu, red[64 + lane]);
             mx = __reduce_max_sync(0xffffffffu, red[96 + lane]);
@@ -1513,16 +1649,15 @@ struct BigLeaf {
                     for (int j = 0; j < BI; ++j)
                         if ((unsigned)eidx(j, off) < (unsigned)m) a[eidx(j, off)] = O::from(xs[j]);
                 }
+                bsync();  // every thread has read lq[0] and lq[1]
                 if (tid == 0) {
-                    sh.lf[k ^ 1] = pend;
+                    sh.lq[0] = sh.lq[1];
+                    sh.lq[1] = sh.lq[2];
                     sh.s_base++;
                     sh.s_bytes += (srcB ? 2ull : 1ull) * 4 * m;
-                    sh.s_cyc_base += clock64() - c0;
+                    sh.s_cyc_base += clock64() - sh.lc0;
                 }
                 bsync();
-                cur = sh.lf[k ^ 1];
-                load(P, cur, xs);
-                k ^= 1;
                 continue;
             }
             const Map mp = make_map(mn, range);
@@ -1535,86 +1670,93 @@ struct BigLeaf {
             }
             bsync();
             uint32_t cmax;
-            {  // (start, count) words: thread t owns buckets [PB t, PB t + PB)
+            {  // (start, count) words: thread t owns buckets [PB t, PB t + PB), scanned in two halves
                 constexpr int PB = BBK / BT;
-                uint32_t cw[PB];
                 uint4 *c4 = reinterpret_cast<uint4 *>(cnt + PB * tid);
+                uint32_t tot = 0, mc = 0;
 #pragma unroll
                 for (int q = 0; q < PB / 4; ++q) {
                     const uint4 y = c4[q];
-                    cw[4 * q] = y.x; cw[4 * q + 1] = y.y; cw[4 * q + 2] = y.z; cw[4 * q + 3] = y.w;
-                }
-                uint32_t tot = 0, mc = 0;
-#pragma unroll
-                for (int q = 0; q < PB; ++q) {
-                    tot += cw[q];
-                    mc = max(mc, cw[q]);
+                    tot += y.x + y.y + y.z + y.w;
+                    mc = max(mc, max(max(y.x, y.y), max(y.z, y.w)));
                 }
                 uint32_t run = block_excl_scan(tot, red, mc, &cmax);
 #pragma unroll
-                for (int q = 0; q < PB; ++q) {
-                    const uint32_t c = cw[q];
-                    cw[q] = run | (c << 16);
-                    run += c;
+                for (int q = 0; q < PB / 4; ++q) {
+                    const uint4 y = c4[q];
+                    uint4 o;
+                    o.x = run | (y.x << 16); run += y.x;
+                    o.y = run | (y.y << 16); run += y.y;
+                    o.z = run | (y.z << 16); run += y.z;
+                    o.w = run | (y.w << 16); run += y.w;
+                    c4[q] = o;
                 }
-#pragma unroll
-                for (int q = 0; q < PB / 4; ++q) c4[q] = make_uint4(cw[4 * q], cw[4 * q + 1], cw[4 * q + 2], cw[4 * q + 3]);
             }
+            if (tid == 0) bulk_wait_read();  // the previous leaf's bulk store has left kc
             bsync();
             PHASE_MARK(1);
+            const uint32_t a0 = (uint32_t)(b & 3);
+            const bool fast = PDQ_BIG_SKIP || cmax <= FAST_CMAX;
 #pragma unroll
             for (int j = 0; j < BI; ++j) {
                 if ((unsigned)eidx(j, off) < (unsigned)m) {
                     PDQ_CHECK(mp(xs[j]) < (uint32_t)BBK, "leaf bucket");
-                    PDQ_CHECK((cnt[mp(xs[j])] & 0xFFFFu) + ((pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu) < (uint32_t)m,
-                              "leaf scatter slot");
-                    kc[(cnt[mp(xs[j])] & 0xFFFFu) + ((pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu)] = xs[j];
+                    const uint32_t p = (cnt[mp(xs[j])] & 0xFFFFu) + ((pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu);
+                    PDQ_CHECK(p < (uint32_t)m, "leaf scatter slot");
+                    kc[fast ? swz(a0 + p) : p] = xs[j];
                 }
-            }
-            const int a0 = (int)(b & 3);
-            if (tid == 0) {
-                bulk_wait_read();  // the previous leaf's bulk store has left kd
-                sh.lf[k ^ 1] = pend;
             }
             bsync();
             PHASE_MARK(2);
-            const uint64_t nxt = sh.lf[k ^ 1];
-            if (cmax <= (uint32_t)CMAX) {
-                load(P, nxt, xs);  // the next leaf's loads fly while this one is ranked and stored
-#pragma unroll
-                for (int j = 0; j < BI; ++j) {  // kc in position order: no per-key state carried over
-                    if (j * BT + tid < m) {
-                        const uint32_t p = j * BT + tid;
-                        const U x = kc[p];
-                        const uint32_t r = rank_in_bucket(kc, x, p, cnt[mp(x)]);
-                        PDQ_CHECK(r < (uint32_t)m, "leaf rank");
-                        kd[a0 + r] = O::from(x);
-                    }
-                }
-            } else {
-                slow_leaf(m, a0, mp, range);
-                load(P, nxt, xs);
-            }
-            fence_proxy_async();
-            bsync();
-            {  // kd[a0, a0 + m) -> A[b, b + m): 16-byte body by one bulk store, head/tail by threads
-                U *a = (U *)P.a_keys + b;
-                int h = (4 - a0) & 3;
-                if (h > m) h = m;
-                const int nb = ((m - h) / 4) * 4;
-                if (tid > 0 && tid < 4 && tid - 1 < h) a[tid - 1] = kd[a0 + tid - 1];
-                if (tid >= 4 && tid < 8 && h + nb + tid - 4 < m) a[h + nb + tid - 4] = kd[a0 + h + nb + tid - 4];
+            if (fast) {
+                window_sort(kc, a0, a0 + (uint32_t)m, (U *)P.a_keys + b);
                 if (tid == 0) {
-                    if (nb) bulk_s2g(a + h, kd + a0 + h, (unsigned)nb * 4u);
-                    bulk_commit();
                     sh.s_base++;
                     sh.s_bytes += 8ull * m;
-                    sh.s_cyc_base += clock64() - c0;
+                    sh.s_cyc_base += clock64() - sh.lc0;
+                    sh.lq[0] = sh.lq[1];
+                    sh.lq[1] = sh.lq[2];
+                }
+                PHASE_MARK(3);
+                bsync();
+                continue;
+            }
+            {
+                // slow path (a bucket of > 13 keys): it needs kd, so the next leaf's prefetch is dropped
+                // (after it lands) and issued again once this leaf's bulk store has read kd
+                if (sh.lq[1] != NONE) {
+                    mbar_wait(bar, kphase);
+                    kphase ^= 1u;
+                }
+                bsync();
+                slow_leaf(m, (int)a0, mp, range);
+            }
+            uint32_t *out = kd;
+            fence_proxy_async();
+            bsync();
+            {  // out[a0, a0 + m) -> A[b, b + m): 16-byte body by one bulk store, head/tail by threads
+                U *a = (U *)P.a_keys + b;
+                int h = (4 - (int)a0) & 3;
+                if (h > m) h = m;
+                const int nb = ((m - h) / 4) * 4;
+                if (tid > 0 && tid < 4 && tid - 1 < h) a[tid - 1] = out[a0 + tid - 1];
+                if (tid >= 4 && tid < 8 && h + nb + tid - 4 < m) a[h + nb + tid - 4] = out[a0 + h + nb + tid - 4];
+                if (tid == 0) {
+                    if (nb) bulk_s2g(a + h, out + a0 + h, (unsigned)nb * 4u);
+                    bulk_commit();
+                    if (sh.lq[1] != NONE) {  // re-issue the dropped prefetch once kd is read
+                        bulk_wait_read();
+                        prefetch(P, sh.lq[1], kd, bar);
+                    }
+                    sh.s_base++;
+                    sh.s_bytes += 8ull * m;
+                    sh.s_cyc_base += clock64() - sh.lc0;
+                    sh.lq[0] = sh.lq[1];
+                    sh.lq[1] = sh.lq[2];
                 }
             }
             PHASE_MARK(3);
-            cur = nxt;
-            k ^= 1;
+            bsync();
         }
         if (tid == 0) bulk_wait_all();
         bsync();

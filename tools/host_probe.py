@@ -1,0 +1,84 @@
+"""Host<->device transfer probe for the drop-in (pageable host buffer) path.
+
+Times, for one 1 GiB int32 host array: the torch pageable copies, cudaHostRegister + pinned DMA,
+and pdq_host_sort's staging pipeline (HostSorter) over thread counts and chunk sizes.
+  python tools/host_probe.py
+"""
+import ctypes
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+n = 1 << 28
+dev = torch.device("cuda:0")
+rng = np.random.default_rng(1)
+host = rng.integers(-(2**31), 2**31, n, dtype=np.int64).astype(np.int32)
+buf = host.copy()
+d = torch.empty(n, dtype=torch.int32, device=dev)
+res = {}
+
+
+def t(f, reps=3):
+    f()
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        f()
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    return best * 1e3
+
+
+res["pageable_h2d_ms"] = t(lambda: d.copy_(torch.from_numpy(buf)))
+res["pageable_d2h_ms"] = t(lambda: torch.from_numpy(buf).copy_(d))
+cudart = torch.cuda.cudart()
+
+
+def reg_roundtrip():
+    p = buf.ctypes.data
+    t0 = time.perf_counter()
+    r = cudart.cudaHostRegister(p, buf.nbytes, 0)
+    t1 = time.perf_counter()
+    d.copy_(torch.from_numpy(buf), non_blocking=True)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    torch.from_numpy(buf).copy_(d, non_blocking=True)
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    cudart.cudaHostUnregister(p)
+    t4 = time.perf_counter()
+    return {"rc": int(r), "register_ms": (t1 - t0) * 1e3, "h2d_ms": (t2 - t1) * 1e3, "d2h_ms": (t3 - t2) * 1e3,
+            "unregister_ms": (t4 - t3) * 1e3}
+
+
+res["host_register"] = [reg_roundtrip() for _ in range(2)]
+
+from paper_2106_05123_b200 import HostSorter  # noqa: E402
+
+exp = np.sort(host)
+rows = []
+for chunk_kb in (2048, 8192, 32768):
+    os.environ["PDQ_HOST_CHUNK_KB"] = str(chunk_kb)
+    for threads in (4, 8, 12, 16):
+        hs = HostSorter(0, threads)
+        best = None
+        for _ in range(3):
+            np.copyto(buf, host)
+            t0 = time.perf_counter()
+            _, ph = hs.sort(buf, phases=True)
+            ms = (time.perf_counter() - t0) * 1e3
+            if best is None or ms < best[0]:
+                best = (ms, ph)
+        ok = bool(np.array_equal(buf, exp))
+        hs.close()
+        rows.append({"chunk_kb": chunk_kb, "threads": threads, "total_ms": best[0], "h2d_ms": best[1][0],
+                     "sort_wait_ms": best[1][1], "d2h_ms": best[1][2], "device_sort_ms": best[1][3], "ok": ok})
+        print(json.dumps(rows[-1]), flush=True)
+res["host_sorter"] = rows
+print(json.dumps(res))
