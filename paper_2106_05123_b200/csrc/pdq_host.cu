@@ -28,7 +28,8 @@
 
 namespace {
 
-constexpr size_t CHUNK_DEFAULT = 8u << 20;  // bytes per staging slot ($PDQ_HOST_CHUNK_KB overrides)
+constexpr size_t CHUNK_DEFAULT = 2u << 20;  // bytes per staging slot ($PDQ_HOST_CHUNK_KB overrides)
+constexpr int MAX_SLOTS = 8;               // staging slots per worker ($PDQ_HOST_SLOTS, default 2)
 
 struct Seg1 {  // one array to transfer: host <-> device, `bytes` long
     unsigned char *host;
@@ -39,8 +40,8 @@ struct Seg1 {  // one array to transfer: host <-> device, `bytes` long
 struct Worker {
     std::thread th;
     cudaStream_t stream = nullptr;
-    unsigned char *slot[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
+    unsigned char *slot[MAX_SLOTS] = {};
+    cudaEvent_t ev[MAX_SLOTS] = {};
     cudaEvent_t done = nullptr;
     int rc = 0;
 };
@@ -55,6 +56,7 @@ struct pdq_host_sorter {
     size_t cap_keys = 0, cap_vals = 0, cap_ws = 0;
     int nthreads = 1;
     size_t chunk = CHUNK_DEFAULT;
+    int nslots = 2;
     std::vector<Worker> w;
     // job dispatch to the worker pool
     std::mutex mu;
@@ -119,11 +121,11 @@ std::vector<ChunkRef> chunk_list(const std::vector<Seg1> &segs, size_t chunk) {
     return out;
 }
 
-// H2D: worker id takes chunks id, id + T, ...; memcpy into slot k while slot k^1's DMA runs
+// H2D: worker id takes chunks id, id + T, ...; memcpy into slot k while the DMAs of its other slots run
 void h2d_worker(pdq_host_sorter *h, int id, const std::vector<ChunkRef> &ch) {
     Worker &w = h->w[id];
     int k = 0;
-    bool used[2] = {false, false};
+    bool used[MAX_SLOTS] = {};
     for (size_t c = id; c < ch.size(); c += h->nthreads) {
         const ChunkRef &r = ch[c];
         if (used[k]) {
@@ -135,31 +137,33 @@ void h2d_worker(pdq_host_sorter *h, int id, const std::vector<ChunkRef> &ch) {
         if (e == cudaSuccess) e = cudaEventRecord(w.ev[k], w.stream);
         if (e != cudaSuccess) { w.rc = fail(h, "h2d copy", e); return; }
         used[k] = true;
-        k ^= 1;
+        k = (k + 1) % h->nslots;
     }
     cudaError_t e = cudaEventRecord(w.done, w.stream);
     if (e != cudaSuccess) w.rc = fail(h, "h2d done", e);
 }
 
-// D2H: DMA chunk c into slot k, then (while the next chunk's DMA runs) memcpy it out
+// D2H: DMAs of the next chunks run into the other slots while chunk i is copied out of its slot
 void d2h_worker(pdq_host_sorter *h, int id, const std::vector<ChunkRef> &ch) {
     Worker &w = h->w[id];
+    const int S = h->nslots;
     cudaError_t e = cudaStreamWaitEvent(w.stream, h->ev_sort, 0);
     if (e != cudaSuccess) { w.rc = fail(h, "d2h wait", e); return; }
     std::vector<size_t> mine;
     for (size_t c = id; c < ch.size(); c += h->nthreads) mine.push_back(c);
     auto issue = [&](size_t i) -> cudaError_t {
         const ChunkRef &r = ch[mine[i]];
-        cudaError_t e2 = cudaMemcpyAsync(w.slot[i & 1], r.s->dev + r.off, r.bytes, cudaMemcpyDeviceToHost, w.stream);
-        if (e2 == cudaSuccess) e2 = cudaEventRecord(w.ev[i & 1], w.stream);
+        cudaError_t e2 = cudaMemcpyAsync(w.slot[i % S], r.s->dev + r.off, r.bytes, cudaMemcpyDeviceToHost, w.stream);
+        if (e2 == cudaSuccess) e2 = cudaEventRecord(w.ev[i % S], w.stream);
         return e2;
     };
-    if (!mine.empty() && (e = issue(0)) != cudaSuccess) { w.rc = fail(h, "d2h copy", e); return; }
+    for (size_t i = 0; i < mine.size() && i + 1 < (size_t)S; ++i)
+        if ((e = issue(i)) != cudaSuccess) { w.rc = fail(h, "d2h copy", e); return; }
     for (size_t i = 0; i < mine.size(); ++i) {
-        if (i + 1 < mine.size() && (e = issue(i + 1)) != cudaSuccess) { w.rc = fail(h, "d2h copy", e); return; }
-        if ((e = cudaEventSynchronize(w.ev[i & 1])) != cudaSuccess) { w.rc = fail(h, "d2h slot wait", e); return; }
+        if (i + S - 1 < mine.size() && (e = issue(i + S - 1)) != cudaSuccess) { w.rc = fail(h, "d2h copy", e); return; }
+        if ((e = cudaEventSynchronize(w.ev[i % S])) != cudaSuccess) { w.rc = fail(h, "d2h slot wait", e); return; }
         const ChunkRef &r = ch[mine[i]];
-        memcpy(r.s->host + r.off, w.slot[i & 1], r.bytes);
+        memcpy(r.s->host + r.off, w.slot[i % S], r.bytes);
     }
 }
 
@@ -191,10 +195,11 @@ extern "C" pdq_host_sorter *pdq_host_sorter_create(int device, int threads) {
         threads = env ? atoi(env) : 0;
         if (threads <= 0) {
             unsigned hw = std::thread::hardware_concurrency();
-            threads = (int)std::min(8u, std::max(1u, hw));
+            threads = (int)std::min(16u, std::max(1u, hw));
         }
     }
     h->nthreads = std::min(threads, 64);
+    if (const char *sl = getenv("PDQ_HOST_SLOTS")) h->nslots = std::max(2, std::min(MAX_SLOTS, atoi(sl)));
     if (const char *ck = getenv("PDQ_HOST_CHUNK_KB")) {
         const long kb = atol(ck);
         if (kb >= 64 && kb <= (256l << 10)) h->chunk = (size_t)kb << 10;
@@ -205,7 +210,7 @@ extern "C" pdq_host_sorter *pdq_host_sorter_create(int device, int threads) {
     h->w.resize(h->nthreads);
     for (Worker &w : h->w) {
         ok = ok && cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking) == cudaSuccess;
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < h->nslots; ++k) {
             ok = ok && cudaHostAlloc((void **)&w.slot[k], h->chunk, cudaHostAllocPortable) == cudaSuccess;
             ok = ok && cudaEventCreateWithFlags(&w.ev[k], cudaEventDisableTiming) == cudaSuccess;
         }
@@ -232,7 +237,7 @@ extern "C" void pdq_host_sorter_destroy(pdq_host_sorter *h) {
     cudaSetDevice(h->device);
     for (Worker &w : h->w) {
         if (w.stream) cudaStreamSynchronize(w.stream), cudaStreamDestroy(w.stream);
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < MAX_SLOTS; ++k) {
             if (w.slot[k]) cudaFreeHost(w.slot[k]);
             if (w.ev[k]) cudaEventDestroy(w.ev[k]);
         }

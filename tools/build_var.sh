@@ -4,7 +4,7 @@
 cd "$(dirname "$0")/.." || exit 1
 name=$1; shift
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -Xptxas -v -Xcompiler -fPIC -shared -std=c++17 -Iinclude \
-  -DPDQ_ONLY_I32 "$@" -o tools/libvar_$name.so paper_2106_05123_b200/csrc/pdq_capi.cu > /tmp/build_$name.log 2>&1
+  -DPDQ_ONLY_I32 "$@" -o tools/libvar_$name.so paper_2106_05123_b200/csrc/pdq_capi.cu paper_2106_05123_b200/csrc/pdq_host.cu > /tmp/build_$name.log 2>&1
 rc=$?; echo "build $name rc=$rc"; grep -E "error" /tmp/build_$name.log | head
 grep -A1 -E "Compiling entry function '_ZN3pdq6k_(sort|base)IjLb0ELb0" /tmp/build_$name.log | grep -o "Used.*" 
 cuobjdump -sass tools/libvar_$name.so > /tmp/var_$name.sass
