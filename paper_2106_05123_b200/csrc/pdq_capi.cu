@@ -60,7 +60,8 @@ namespace {
 constexpr int MIN_BASE = 1024;
 
 struct Layout {
-    size_t b_keys, b_vals, state, segs, ring, leaves, total;
+    size_t b_keys, b_vals, state, segs, ring, leaves, rslots, total;
+    uint32_t rslot_cap;
     uint64_t leaf_cap;
     uint32_t seg_cap;
     int log_q;
@@ -105,6 +106,11 @@ Layout layout(int dtype, int has_payload, int64_t n) {
     L.leaf_cap = (uint64_t)n / 64 + 16;
     L.leaves = off;
     off += a256((size_t)L.leaf_cap * 8);
+    // K5 digit passes: one slot of RDIG 64-bit counters per radix segment (bump-allocated; when they
+    // run out a segment falls back to one-bit radix exchange, which needs none)
+    L.rslot_cap = (uint32_t)((uint64_t)n / 8192 + 512);
+    L.rslots = off;
+    off += a256((size_t)L.rslot_cap * RDIG * 8);
     L.total = off;
     return L;
 }
@@ -277,6 +283,8 @@ extern "C" int pdq_sort_timed(void *keys, int dtype, uint32_t *payload, int64_t 
     P.debug_depth = cfg.reserved[0];
     P.leaves = (uint64_t *)(ws + L.leaves);
     P.leaf_cap = L.leaf_cap;
+    P.rslots = (unsigned long long *)(ws + L.rslots);
+    P.rslot_cap = L.rslot_cap;
 
 
     const bool kv = payload != nullptr;

@@ -30,7 +30,7 @@ constexpr int64_t INLINE_FILL = 16 * TILE;  // fills up to this size run inline 
 // ---- task ring --------------------------------------------------------------------
 // A task is one 64-bit word carrying its own round tag, so publishing it is a
 // single store:  [63:48] round tag | [47:45] type | [44:23] segment | [22:0] tile.
-enum : uint32_t { T_PART = 1, T_FILL = 2 };
+enum : uint32_t { T_PART = 1, T_FILL = 2, T_RHIST = 3, T_RSCAT = 4 };  // RHIST/RSCAT: K5 digit passes
 __host__ __device__ inline uint64_t task_word(uint64_t pos, int log_q, uint32_t type, uint32_t seg,
                                               uint32_t tile) {
     return ((pos >> log_q) & 0xFFFFull) << 48 | (uint64_t)(type & 7) << 45 |
@@ -49,7 +49,9 @@ enum : uint32_t {
     I_COUNT_EQ = 1u << 4, // the sample's low end repeats the pivot: count keys equal to it
     I_RADIX = 1u << 5,    // K5 fallback: radix exchange on composite bit `rbit` (threshold pivot)
     I_HAS_UB = 1u << 6,   // `ub` is a valid exclusive upper bound
+    I_RADIX8 = 1u << 7,   // K5 fallback: 8-bit digit pass on composite bits [rbit, rbit + 8) (slot `rslot`)
 };
+constexpr int RDIG = 256;  // digits of a K5 radix pass
 
 struct __align__(128) Seg {
     int64_t begin, end;   // [begin, end) in element indices
@@ -66,7 +68,7 @@ struct __align__(128) Seg {
     unsigned int tiles_done;
     unsigned int rbit;    // I_RADIX: the composite bit this split decides (0 = most significant)
     uint32_t ub_v;
-    uint32_t pad0;
+    uint32_t rslot;       // I_RADIX8: the segment's 256-counter slot (histogram, then scatter cursors)
     uint64_t ub;          // exclusive upper bound (ordered), valid iff I_HAS_UB
     uint64_t pad1;
 };
@@ -84,7 +86,7 @@ struct __align__(128) State {
     int status;
     unsigned int check_bits;       // K4: 1 descent seen, 2 ascent seen
     unsigned int reverse;          // K4 decided the input is non-increasing
-    unsigned int pad_c;
+    unsigned int rslot_alloc;      // K5 radix-slot bump allocator
     unsigned long long pad_d[12];
     // counters (pdq_stats order)
     unsigned long long leaf_count;  // queued base-case segments (K7 kernel input)
@@ -116,6 +118,8 @@ struct Params {
     uint64_t *leaves;  // queued leaves: begin << 16 | (size - 1) << 1 | in-B
     unsigned long long leaf_cap;
     uint32_t chunk;    // tiles per ring task
+    unsigned long long *rslots;  // K5: rslot_cap slots of RDIG counters
+    uint32_t rslot_cap;
 };
 
 // ---- key traits ----------------------------------------------------------------------

@@ -26,7 +26,43 @@
 
 #include "../../include/pdq_b200.h"
 
+#if defined(__x86_64__)
+#include <emmintrin.h>
+#endif
+
 namespace {
+
+// memcpy with non-temporal (streaming) stores: the destination (a pinned slot about to be DMA'd, or
+// the caller's buffer) is not read back by this CPU, so streaming stores skip the read-for-ownership
+// of every destination line -- a third of the host memory traffic of a staged copy.
+// $PDQ_HOST_NT=0 uses plain memcpy.
+bool g_nt = true;
+void copy_nt(unsigned char *dst, const unsigned char *src, size_t n) {
+#if defined(__x86_64__)
+    if (g_nt && n >= 4096) {
+        size_t h = (16 - ((uintptr_t)dst & 15)) & 15;
+        memcpy(dst, src, h);
+        dst += h;
+        src += h;
+        n -= h;
+        size_t i = 0;
+        for (; i + 64 <= n; i += 64) {
+            const __m128i a = _mm_loadu_si128((const __m128i *)(src + i));
+            const __m128i b = _mm_loadu_si128((const __m128i *)(src + i + 16));
+            const __m128i c = _mm_loadu_si128((const __m128i *)(src + i + 32));
+            const __m128i d = _mm_loadu_si128((const __m128i *)(src + i + 48));
+            _mm_stream_si128((__m128i *)(dst + i), a);
+            _mm_stream_si128((__m128i *)(dst + i + 16), b);
+            _mm_stream_si128((__m128i *)(dst + i + 32), c);
+            _mm_stream_si128((__m128i *)(dst + i + 48), d);
+        }
+        _mm_sfence();
+        memcpy(dst + i, src + i, n - i);
+        return;
+    }
+#endif
+    memcpy(dst, src, n);
+}
 
 constexpr size_t CHUNK_DEFAULT = 2u << 20;  // bytes per staging slot ($PDQ_HOST_CHUNK_KB overrides)
 constexpr int MAX_SLOTS = 8;               // staging slots per worker ($PDQ_HOST_SLOTS, default 2)
@@ -132,7 +168,7 @@ void h2d_worker(pdq_host_sorter *h, int id, const std::vector<ChunkRef> &ch) {
             cudaError_t e = cudaEventSynchronize(w.ev[k]);  // the slot's previous DMA has read it
             if (e != cudaSuccess) { w.rc = fail(h, "h2d slot wait", e); return; }
         }
-        memcpy(w.slot[k], r.s->host + r.off, r.bytes);
+        copy_nt(w.slot[k], r.s->host + r.off, r.bytes);
         cudaError_t e = cudaMemcpyAsync(r.s->dev + r.off, w.slot[k], r.bytes, cudaMemcpyHostToDevice, w.stream);
         if (e == cudaSuccess) e = cudaEventRecord(w.ev[k], w.stream);
         if (e != cudaSuccess) { w.rc = fail(h, "h2d copy", e); return; }
@@ -163,7 +199,7 @@ void d2h_worker(pdq_host_sorter *h, int id, const std::vector<ChunkRef> &ch) {
         if (i + S - 1 < mine.size() && (e = issue(i + S - 1)) != cudaSuccess) { w.rc = fail(h, "d2h copy", e); return; }
         if ((e = cudaEventSynchronize(w.ev[i % S])) != cudaSuccess) { w.rc = fail(h, "d2h slot wait", e); return; }
         const ChunkRef &r = ch[mine[i]];
-        memcpy(r.s->host + r.off, w.slot[i % S], r.bytes);
+        copy_nt(r.s->host + r.off, w.slot[i % S], r.bytes);
     }
 }
 
@@ -199,6 +235,7 @@ extern "C" pdq_host_sorter *pdq_host_sorter_create(int device, int threads) {
         }
     }
     h->nthreads = std::min(threads, 64);
+    if (const char *nt = getenv("PDQ_HOST_NT")) g_nt = atoi(nt) != 0;
     if (const char *sl = getenv("PDQ_HOST_SLOTS")) h->nslots = std::max(2, std::min(MAX_SLOTS, atoi(sl)));
     if (const char *ck = getenv("PDQ_HOST_CHUNK_KB")) {
         const long kb = atol(ck);
@@ -276,7 +313,10 @@ extern "C" int pdq_host_sort(pdq_host_sorter *h, void *keys, int dtype, uint32_t
 
     std::vector<Seg1> segs{{(unsigned char *)keys, h->d_keys, kb}};
     if (payload) segs.push_back({(unsigned char *)payload, h->d_vals, vb});
-    const std::vector<ChunkRef> ch = chunk_list(segs, h->chunk);
+    // chunks: the slot size, or smaller so that a small array still spreads over every worker
+    size_t ck = (kb + vb + h->nthreads - 1) / h->nthreads;
+    ck = std::max<size_t>(64u << 10, std::min(h->chunk, (ck + (64u << 10) - 1) & ~(size_t)((64u << 10) - 1)));
+    const std::vector<ChunkRef> ch = chunk_list(segs, ck);
     for (Worker &wk : h->w) wk.rc = 0;
 
     // 1. H2D through the pinned slots (all workers)

@@ -81,6 +81,7 @@ struct Shared {
     int wl[WARPS], weq[WARPS];
     long long L, R, lOff, rOff, fL, fE;
     int aL, aR;  // kc positions of the current tile's left / right runs
+    int rl_tiny, rl_seq;     // K5 finalizer: children sorted by warps / handled by the whole CTA
     unsigned long long push_pos;
     uint32_t new_sid;
     int last;
@@ -154,7 +155,9 @@ struct Sorter {
     
     static constexpr int KBITS = 8 * (int)sizeof(U);
     static constexpr int NBITS = KBITS + (KV ? 32 : 0);  // bits of the (ordered key, payload) composite
-    __device__ __forceinline__ static bool tile_task(uint32_t type) { return type == T_PART; }
+    __device__ __forceinline__ static bool tile_task(uint32_t type) {
+        return type == T_PART || type == T_RHIST || type == T_RSCAT;
+    }
 
     // Bounds known for a segment: every element e satisfies lb <= e (has_lb) and e < ub (has_ub),
     // in the (ordered key, payload) order.  lb is the reference's predecessor (driver.py:222).
@@ -334,10 +337,11 @@ struct Sorter {
         Shared &sh = g_sh;
         const unsigned long long pos = sh.push_pos;
         const uint64_t mask = (1ull << P.log_q) - 1;
-        const uint32_t nt = type == T_PART ? seg_ntasks(ntiles, P.chunk) : ntiles;
+        const bool chunked = tile_task(type);
+        const uint32_t nt = chunked ? seg_ntasks(ntiles, P.chunk) : ntiles;
         for (uint32_t t = threadIdx.x; t < nt; t += THREADS)
             *(volatile uint64_t *)&P.ring[(pos + t) & mask] =
-                task_word(pos + t, P.log_q, type, sid, type == T_PART ? t * P.chunk : t);
+                task_word(pos + t, P.log_q, type, sid, chunked ? t * P.chunk : t);
     }
 
     // ---- write [b, e) of A with the pivot (equal-key runs are bitwise identical under the
@@ -508,7 +512,7 @@ struct Sorter {
                     pv = (KV && bit > KBITS) ? (bit - KBITS >= 32 ? bd.lbv : (bd.lbv & ~(0xFFFFFFFFu >> (bit - KBITS)))) : 0u;
                 }
             }
-            return radix_split(P, b, e, srcB, bit, pk, pv, depth, reuse_sid);
+            return radix8_start(P, b, e, srcB, bit, pk, pv, depth, reuse_sid);
         }
         // K1: stratified samples (64, or SAMPLES for segments of 2^20+ keys); perturbed strata
         // after a bad partition.  The median of the sorted sample is the pivot.
@@ -687,8 +691,438 @@ struct Sorter {
         }
     }
 
+    // ---- K5: 8-bit digit passes (the role of heapsort, driver.py:209-213; small_sorts.py:134-154) ------
+    // A segment whose bad-partition budget is spent leaves quicksort for MSD radix passes over the bits of
+    // its (ordered key, payload) composite below the prefix its bounds already fix.  One pass = a
+    // histogram over the segment's tiles (T_RHIST: w bytes read per element, or w + 4 once the digit
+    // reaches the payload) into the segment's slot of 256 counters, an exclusive scan into scatter cursors
+    // (the finalizer), and a scatter over the same tiles (T_RSCAT: 2 (w + p) bytes per element): each
+    // tile is reordered by digit in its own stage, reserves one run per digit with one atomic on that
+    // digit's cursor, and writes its runs to the other buffer.  The 256 children then become leaves or
+    // radix segments on the next 8 bits -- the work is bounded by the key width, never quadratic.  A pass
+    // whose histogram finds a single digit skips the scatter.  (Bits are MSB-first composite positions.)
+    __device__ __forceinline__ static int rdigits(int rbit) { return NBITS - rbit < 8 ? NBITS - rbit : 8; }
+    __device__ __forceinline__ static bool hist_keys_only(uint64_t task, const Seg &sg) {
+        return ((uint32_t)(task >> 45) & 7u) == T_RHIST && (int)sg.rbit + rdigits((int)sg.rbit) <= KBITS;
+    }
+    __device__ __forceinline__ static uint32_t digit_of(U k, uint32_t v, int rbit, int nd) {
+        const uint32_t mask = (1u << nd) - 1u;
+        if (rbit + nd <= KBITS) return (uint32_t)((uint64_t)k >> (KBITS - rbit - nd)) & mask;
+        if (rbit >= KBITS) return (v >> (32 - (rbit - KBITS) - nd)) & mask;
+        const int kb = KBITS - rbit, vb = nd - kb;
+        return ((((uint32_t)(uint64_t)k) & ((1u << kb) - 1u)) << vb) | (v >> (32 - vb));
+    }
+    // the prefix (pk, pv) with digit dv at composite bits [rbit, rbit + nd)
+    __device__ __forceinline__ static void put_digit(uint64_t &pk, uint32_t &pv, int rbit, int nd, uint32_t dv) {
+        if (rbit + nd <= KBITS) {
+            pk |= (uint64_t)dv << (KBITS - rbit - nd);
+        } else if (rbit >= KBITS) {
+            pv |= dv << (32 - (rbit - KBITS) - nd);
+        } else {
+            const int kb = KBITS - rbit, vb = nd - kb;
+            pk |= (uint64_t)(dv >> vb);
+            pv |= (dv & ((1u << vb) - 1u)) << (32 - vb);
+        }
+    }
+    // warp-aggregated shared-memory counter increment: one atomic when every valid lane has the same digit
+    __device__ __forceinline__ static uint32_t count_digit(uint32_t *cnt, bool valid, uint32_t d) {
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        if (!vm) return 0;
+        const int lead = __ffs(vm) - 1;
+        const uint32_t d0 = __shfl_sync(0xffffffffu, d, lead);
+        if (__all_sync(0xffffffffu, !valid || d == d0)) {
+            uint32_t base = 0;
+            if ((int)(threadIdx.x & 31) == lead) base = atomicAdd(&cnt[d0], (uint32_t)__popc(vm));
+            base = __shfl_sync(0xffffffffu, base, lead);
+            return base + (uint32_t)__popc(vm & lanemask_lt());
+        }
+        return valid ? atomicAdd(&cnt[d], 1u) : 0u;
+    }
+
+    // T_RHIST tile: digit histogram of the tile, added to the segment's slot (kc holds the counters)
+    __device__ static void hist_tile(const Params &P, uint32_t tile, unsigned &ci) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x;
+        const Seg &sg = sh.seg;
+        const int64_t b = sg.begin, e = sg.end;
+        const int64_t tbase = (b / TL + tile) * (int64_t)TL;
+        const int lo_i = (int)((b > tbase ? b : tbase) - tbase), hi_i = (int)((e < tbase + TL ? e : tbase + TL) - tbase);
+        const int st = (int)(ci % B::NSTAGE);
+        const U *sk = B::stage(st);
+        const uint32_t *sv = KV ? B::vstage(st) : nullptr;
+        const int rbit = (int)sg.rbit, nd = rdigits(rbit);
+        uint32_t *cnt = reinterpret_cast<uint32_t *>(B::kc());
+        cnt[tid] = 0;  // THREADS == RDIG
+        mbar_wait(&sh.bar[st], (ci / B::NSTAGE) & 1u);
+        ++ci;
+        csync();
+        for (int i0 = lo_i; i0 < hi_i; i0 += THREADS) {
+            const int i = i0 + tid;
+            const bool valid = i < hi_i;
+            uint32_t d = 0;
+            if (valid) d = digit_of(O::to(sk[i]), (KV && rbit + nd > KBITS) ? sv[i] : 0u, rbit, nd);
+            count_digit(cnt, valid, d);
+        }
+        csync();  // histogram complete, stage consumed
+        if (tid == 0) {
+            sh.ci = ci;
+            pump_loads(P);
+            sh.s_tiles++;
+            sh.s_bytes += (unsigned long long)(hi_i - lo_i) * (rbit + nd <= KBITS ? sizeof(U) : ELEM_BYTES);
+        }
+        const uint32_t c = cnt[tid];
+        if (c) atomicAdd(&P.rslots[(size_t)sg.rslot * RDIG + tid], (unsigned long long)c);
+        csync();  // kc is free again
+    }
+
+    // T_RSCAT tile: reorder the tile by digit in its own stage, reserve one run per digit, write the runs
+    __device__ static void rscat_tile(const Params &P, uint32_t tile, unsigned &ci) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        const Seg &sg = sh.seg;
+        const int64_t b = sg.begin, e = sg.end;
+        const int64_t tbase = (b / TL + tile) * (int64_t)TL;
+        const int lo_i = (int)((b > tbase ? b : tbase) - tbase), hi_i = (int)((e < tbase + TL ? e : tbase + TL) - tbase);
+        const int st = (int)(ci % B::NSTAGE);
+        U *sk = B::stage(st);
+        uint32_t *sv = KV ? B::vstage(st) : nullptr;
+        const int rbit = (int)sg.rbit, nd = rdigits(rbit);
+        const bool srcB = sg.info & I_SRC_B;
+        U *dst = (U *)(srcB ? P.a_keys : P.b_keys);
+        uint32_t *dstv = srcB ? P.a_vals : P.b_vals;
+        uint32_t *cnt = reinterpret_cast<uint32_t *>(B::kc());
+        uint32_t *lst = cnt + RDIG;
+        long long *gd = reinterpret_cast<long long *>(cnt + 2 * RDIG);
+        uint32_t *wsum = cnt + 4 * RDIG;
+        cnt[tid] = 0;
+        mbar_wait(&sh.bar[st], (ci / B::NSTAGE) & 1u);
+        ++ci;
+        csync();
+        U kx[IT];
+        uint32_t vx[IT], pk[IT];
+#pragma unroll
+        for (int r = 0; r < IT; ++r) {
+            const int i = r * THREADS + tid;
+            const bool valid = i >= lo_i && i < hi_i;
+            kx[r] = valid ? sk[i] : (U)0;
+            vx[r] = (KV && valid) ? sv[i] : 0u;
+            const uint32_t d = valid ? digit_of(O::to(kx[r]), vx[r], rbit, nd) : 0u;
+            const uint32_t sl = count_digit(cnt, valid, d);
+            pk[r] = valid ? (d << 16 | sl) : 0xFFFFFFFFu;
+        }
+        csync();
+        {  // digit t = thread t: exclusive scan of the tile's counts, then one cursor atomic per digit
+            const uint32_t c = cnt[tid];
+            uint32_t inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane == 31) wsum[warp] = inc;
+            csync();
+            uint32_t wpre = 0;
+#pragma unroll
+            for (int w = 0; w < WARPS; ++w) wpre += (w < warp) ? wsum[w] : 0u;
+            const uint32_t ex = wpre + inc - c;
+            lst[tid] = ex;
+            long long g = 0;
+            if (c) g = (long long)atomicAdd(&P.rslots[(size_t)sg.rslot * RDIG + tid], (unsigned long long)c);
+            gd[tid] = g - (long long)ex;
+        }
+        csync();  // every input element is in registers: the stage is rewritten in digit order
+#pragma unroll
+        for (int r = 0; r < IT; ++r) {
+            if (pk[r] != 0xFFFFFFFFu) {
+                const uint32_t pos = lst[pk[r] >> 16] + (pk[r] & 0xFFFFu);
+                sk[pos] = kx[r];
+                if (KV) sv[pos] = vx[r];
+            }
+        }
+        csync();
+        const int nv = hi_i - lo_i;
+        for (int p = tid; p < nv; p += THREADS) {  // consecutive threads write consecutive slots of a run
+            const U k = sk[p];
+            const uint32_t v = KV ? sv[p] : 0u;
+            const long long g = gd[digit_of(O::to(k), v, rbit, nd)] + p;
+            dst[g] = k;
+            if (KV) dstv[g] = v;
+        }
+        csync();  // stage consumed, kc free
+        if (tid == 0) {
+            sh.ci = ci;
+            pump_loads(P);
+            sh.s_tiles++;
+            sh.s_bytes += 2ull * ELEM_BYTES * (unsigned long long)nv;
+        }
+    }
+
+    // one warp sorts [b, b + m), m <= 64, from buffer srcB into A (tiny_sort for any warp)
+    __device__ static void tiny_sort_warp(const Params &P, bool srcB, int64_t b, int m) {
+        Shared &sh = g_sh;
+        const int lane = threadIdx.x & 31;
+        const U *src = (const U *)(srcB ? P.b_keys : P.a_keys);
+        const uint32_t *srcv = srcB ? P.b_vals : P.a_vals;
+        uint64_t x[2];
+        uint32_t y[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int i = 2 * lane + q;
+            x[q] = i < m ? (uint64_t)O::to(ldcg(src + b + i)) : ~0ull;
+            y[q] = (KV && i < m) ? ldcg(srcv + b + i) : 0xFFFFFFFFu;
+        }
+        warp_bitonic<2>(x, y);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int i = 2 * lane + q;
+            if (i < m) {
+                ((U *)P.a_keys)[b + i] = O::from((U)x[q]);
+                if (KV) P.a_vals[b + i] = y[q];
+            }
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+            atomicAdd(&sh.s_base, 1ull);
+            atomicAdd(&sh.s_bytes, 2ull * ELEM_BYTES * m);
+            finish_keys(P, (unsigned long long)m);
+        }
+    }
+
+    // Start a digit-pass segment [b, e) in buffer srcB on composite bit `bit` with known prefix (pk, pv).
+    // Falls back to one-bit radix exchange when the radix slots are exhausted.  Returns true iff the
+    // reusable descriptor was consumed.
+    __device__ static bool radix8_start(const Params &P, int64_t b, int64_t e, bool srcB, int bit, uint64_t pk,
+                                        uint32_t pv, int depth, int reuse_sid) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x;
+        const int64_t m = e - b;
+        if (m <= 0) return false;
+        if (bit >= NBITS || m == 1) {
+            finish_constant(P, b, e, srcB);
+            return false;
+        }
+        if (m <= P.base_size) {
+            Bnd nb{};
+            return spawn(P, b, e, srcB, nb, 1, depth, false, reuse_sid);  // leaf
+        }
+        if (tid == 0) sh.new_sid = atomicAdd(&P.st->rslot_alloc, 1u);
+        csync();
+        const uint32_t slot = sh.new_sid;
+        csync();
+        if (slot >= P.rslot_cap) return radix_split(P, b, e, srcB, bit, pk, pv, depth, reuse_sid);
+        P.rslots[(size_t)slot * RDIG + tid] = 0ull;  // THREADS == RDIG
+        __threadfence();
+        csync();
+        const uint32_t ntiles = (uint32_t)((e - 1) / TL - b / TL + 1);
+        if (tid == 0) {
+            const uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
+            sh.new_sid = sid;
+            if (sid >= P.seg_cap) {
+                fail(P, -6);
+            } else {
+                Seg *s = &P.segs[sid];
+                s->begin = b;
+                s->end = e;
+                s->pivot = 0;
+                s->pivot_v = 0;
+                s->lb = pk;
+                s->lb_v = pv;
+                s->ntiles = ntiles;
+                s->info = (srcB ? I_SRC_B : 0) | I_RADIX8;
+                s->rbit = (unsigned)bit;
+                s->rslot = slot;
+                s->budget = 0;
+                s->depth = depth;
+                s->cnt_left = 0;
+                s->cnt_right = 0;
+                s->cnt_eq = 0;
+                s->tiles_done = 0;
+                __threadfence();
+                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)seg_ntasks(ntiles, P.chunk));
+            }
+            if (depth > sh.s_max_depth) sh.s_max_depth = depth;
+        }
+        csync();
+        if (sh.new_sid < P.seg_cap) push_tasks(P, T_RHIST, sh.new_sid, ntiles);
+        csync();
+        return reuse_sid >= 0;
+    }
+
+    // 64-bit exclusive scan of one value per thread (CTA-wide; contains barriers)
+    __device__ __forceinline__ static unsigned long long block_excl_u64(unsigned long long v) {
+        Shared &sh = g_sh;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        unsigned long long inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) sh.red_max[warp] = inc;
+        csync();
+        unsigned long long pre = 0;
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) pre += (w < warp) ? sh.red_max[w] : 0ull;
+        csync();
+        return pre + inc - v;
+    }
+
+    // the histogram of a digit pass is complete: turn it into scatter cursors (or skip a one-digit pass)
+    __device__ __noinline__ static void radix_hist_done(const Params &P, const Seg &sg, uint32_t sid) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x;
+        unsigned long long *cs = P.rslots + (size_t)sg.rslot * RDIG;
+        const int64_t b = sg.begin, e = sg.end, m = e - b;
+        const bool srcB = sg.info & I_SRC_B;
+        const int rbit = (int)sg.rbit, nd = rdigits(rbit);
+        const unsigned long long c = __ldcg(&cs[tid]);
+        const unsigned long long ex = block_excl_u64(c);
+        if (c == (unsigned long long)m) sh.aL = tid;  // the one digit every element has
+        if (tid == 0) sh.s_part_right++;
+        if (csync_or(c == (unsigned long long)m)) {
+            uint64_t pk = sg.lb;
+            uint32_t pv = sg.lb_v;
+            put_digit(pk, pv, rbit, nd, (uint32_t)sh.aL);
+            if (rbit + nd >= NBITS) {
+                finish_constant(P, b, e, srcB);
+                return;
+            }
+            cs[tid] = 0ull;  // the next digit's histogram, same segment, same buffer
+            __threadfence();
+            csync();
+            if (tid == 0) {
+                Seg *gs = &P.segs[sid];
+                gs->rbit = (unsigned)(rbit + nd);
+                gs->lb = pk;
+                gs->lb_v = pv;
+                gs->tiles_done = 0;
+                __threadfence();
+                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)seg_ntasks(sg.ntiles, P.chunk));
+            }
+            csync();
+            push_tasks(P, T_RHIST, sid, sg.ntiles);
+            csync();
+            return;
+        }
+        cs[tid] = (unsigned long long)b + ex;  // scatter cursor of digit tid
+        __threadfence();
+        csync();
+        if (tid == 0) {
+            P.segs[sid].tiles_done = 0;
+            __threadfence();
+            sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)seg_ntasks(sg.ntiles, P.chunk));
+        }
+        csync();
+        push_tasks(P, T_RSCAT, sid, sg.ntiles);
+        csync();
+    }
+
+    // the scatter of a digit pass is complete: the 256 digit runs are the children (thread t: digit t)
+    __device__ __noinline__ static void radix_scat_done(const Params &P, const Seg &sg, uint32_t sid) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x, warp = tid >> 5;
+        unsigned long long *cs = P.rslots + (size_t)sg.rslot * RDIG;
+        unsigned long long *E = reinterpret_cast<unsigned long long *>(B::kc());  // run ends
+        uint8_t *tiny = reinterpret_cast<uint8_t *>(E + RDIG), *seq = tiny + RDIG;
+        E[tid] = __ldcg(&cs[tid]);
+        if (tid == 0) {
+            sh.rl_tiny = 0;
+            sh.rl_seq = 0;
+        }
+        csync();
+        const int rbit = (int)sg.rbit, nd = rdigits(rbit), nrbit = rbit + nd;
+        const bool dstB = !(sg.info & I_SRC_B);
+        const int64_t cb = tid ? (int64_t)E[tid - 1] : sg.begin, ce = (int64_t)E[tid], mc = ce - cb;
+        uint64_t pk = sg.lb;
+        uint32_t pv = sg.lb_v;
+        put_digit(pk, pv, rbit, nd, (uint32_t)tid);
+        if (mc == 1) {
+            if (dstB) {
+                ((U *)P.a_keys)[cb] = ldcg((const U *)P.b_keys + cb);
+                if (KV) P.a_vals[cb] = ldcg(P.b_vals + cb);
+                atomicAdd(&sh.s_bytes, 2ull * ELEM_BYTES);
+                __threadfence();
+            }
+            finish_keys(P, 1ull);
+        } else if (mc > 1 && nrbit >= NBITS && !dstB) {
+            finish_keys(P, (unsigned long long)mc);  // every bit decided: a constant run, already in A
+        } else if (mc > 1 && mc <= 64 && nrbit < NBITS) {
+            tiny[atomicAdd(&sh.rl_tiny, 1)] = (uint8_t)tid;
+        } else if (mc > 1 && mc <= P.base_size) {
+            // a leaf for the base-case kernel (a constant run in B is copied by it as well)
+            const unsigned long long pos = atomicAdd(&P.st->leaf_count, 1ull);
+            if (pos < P.leaf_cap)
+                P.leaves[pos] = (uint64_t)cb << 16 | (uint64_t)(mc - 1) << 1 | (dstB ? 1u : 0u);
+            else
+                fail(P, -6);
+            finish_keys(P, (unsigned long long)mc);
+        } else if (mc > 1 && nrbit < NBITS) {
+            // a radix segment on the next digit
+            const uint32_t slot = atomicAdd(&P.st->rslot_alloc, 1u);
+            const uint32_t csid = slot < P.rslot_cap ? atomicAdd(&P.st->seg_alloc, 1u) : 0xFFFFFFFFu;
+            if (slot >= P.rslot_cap) {
+                seq[atomicAdd(&sh.rl_seq, 1)] = (uint8_t)tid;
+            } else if (csid >= P.seg_cap) {
+                fail(P, -6);
+            } else {
+                unsigned long long *ccs = P.rslots + (size_t)slot * RDIG;
+                for (int q = 0; q < RDIG; ++q) ccs[q] = 0ull;
+                const uint32_t ntiles = (uint32_t)((ce - 1) / TL - cb / TL + 1);
+                Seg *s = &P.segs[csid];
+                s->begin = cb;
+                s->end = ce;
+                s->pivot = 0;
+                s->pivot_v = 0;
+                s->lb = pk;
+                s->lb_v = pv;
+                s->ntiles = ntiles;
+                s->info = (dstB ? I_SRC_B : 0) | I_RADIX8;
+                s->rbit = (unsigned)nrbit;
+                s->rslot = slot;
+                s->budget = 0;
+                s->depth = sg.depth + 1;
+                s->cnt_left = 0;
+                s->cnt_right = 0;
+                s->cnt_eq = 0;
+                s->tiles_done = 0;
+                __threadfence();
+                const uint32_t nt = seg_ntasks(ntiles, P.chunk);
+                const unsigned long long pos = atomicAdd(&P.st->q_tail, (unsigned long long)nt);
+                const uint64_t mask = (1ull << P.log_q) - 1;
+                for (uint32_t t = 0; t < nt; ++t)
+                    *(volatile uint64_t *)&P.ring[(pos + t) & mask] =
+                        task_word(pos + t, P.log_q, T_RHIST, csid, t * P.chunk);
+                atomicMax(&sh.s_max_depth, (long long)(sg.depth + 1));
+            }
+        } else if (mc > 1) {
+            seq[atomicAdd(&sh.rl_seq, 1)] = (uint8_t)tid;  // a constant run in B longer than a leaf
+        }
+        csync();
+        for (int i = warp; i < sh.rl_tiny; i += WARPS) {
+            const int d = tiny[i];
+            const int64_t tb = d ? (int64_t)E[d - 1] : sg.begin;
+            tiny_sort_warp(P, dstB, tb, (int)((int64_t)E[d] - tb));
+        }
+        csync();
+        const int nseq = sh.rl_seq;
+        for (int i = 0; i < nseq; ++i) {
+            const int d = seq[i];
+            const int64_t tb = d ? (int64_t)E[d - 1] : sg.begin, te = (int64_t)E[d];
+            if (nrbit >= NBITS) {
+                finish_constant(P, tb, te, dstB);
+            } else {
+                uint64_t qk = sg.lb;
+                uint32_t qv = sg.lb_v;
+                put_digit(qk, qv, rbit, nd, (uint32_t)d);
+                radix_split(P, tb, te, dstB, nrbit, qk, qv, sg.depth + 1, -1);
+            }
+        }
+        csync();
+    }
+
     // ---- thread 0: issue the TMA bulk load of tile `tile` of segment `sg` into the next stage ----------
-    __device__ static void issue_load(const Params &P, const Seg &sg, uint32_t tile) {
+    __device__ static void issue_load(const Params &P, const Seg &sg, uint32_t tile, bool keys_only = false) {
         Shared &sh = g_sh;
         const int st = (int)(sh.li % B::NSTAGE);
         ++sh.li;
@@ -708,15 +1142,15 @@ struct Sorter {
         // the array's last < 16 bytes cannot be bulk-copied: scalar loads
         for (int64_t g = (hi_al > lo ? hi_al : lo); g < hi; ++g) {
             sk[g - tbase] = ldcg(src + g);
-            if (KV) sv[g - tbase] = ldcg(srcv + g);
+            if (KV && !keys_only) sv[g - tbase] = ldcg(srcv + g);
         }
         const unsigned kb = hi_al > lo_al ? (unsigned)((hi_al - lo_al) * sizeof(U)) : 0u;
-        const unsigned vb = (KV && hi_al > lo_al) ? (unsigned)((hi_al - lo_al) * 4) : 0u;
+        const unsigned vb = (KV && !keys_only && hi_al > lo_al) ? (unsigned)((hi_al - lo_al) * 4) : 0u;
         fence_proxy_async();
         mbar_expect_tx(&sh.bar[st], kb + vb);  // the stage barrier's single arrival (+ bytes, maybe 0)
         if (kb) {
             bulk_g2s(sk + (lo_al - tbase), src + lo_al, kb, &sh.bar[st]);
-            if (KV) bulk_g2s(sv + (lo_al - tbase), srcv + lo_al, vb, &sh.bar[st]);
+            if (vb) bulk_g2s(sv + (lo_al - tbase), srcv + lo_al, vb, &sh.bar[st]);
         }
     }
 
@@ -991,7 +1425,7 @@ struct Sorter {
                 if (sh.task && tile_task((uint32_t)(sh.task >> 45) & 7u)) {
                     const uint32_t end = task_end_tile((uint32_t)(sh.task & 0x7FFFFF), sh.seg.ntiles, P.chunk);
                     if (sh.ltile < end) {
-                        issue_load(P, sh.seg, sh.ltile++);
+                        issue_load(P, sh.seg, sh.ltile++, hist_keys_only(sh.task, sh.seg));
                         continue;
                     }
                 }
@@ -1005,7 +1439,7 @@ struct Sorter {
             if (!tile_task((uint32_t)(sh.ntask >> 45) & 7u)) return;
             const uint32_t end = task_end_tile((uint32_t)(sh.ntask & 0x7FFFFF), sh.nseg.ntiles, P.chunk);
             if (sh.ltile >= end) return;
-            issue_load(P, sh.nseg, sh.ltile++);
+            issue_load(P, sh.nseg, sh.ltile++, hist_keys_only(sh.ntask, sh.nseg));
         }
     }
 
@@ -2228,10 +2662,16 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
         if (!w) break;
         const uint32_t type = (uint32_t)(w >> 45) & 7u;
         const uint32_t sid = (uint32_t)(w >> 23) & 0x3FFFFF;
-        if (type == T_PART) {
+        if (S::tile_task(type)) {
             const uint32_t t0 = (uint32_t)w & 0x7FFFFF;
             const uint32_t t1 = task_end_tile(t0, sh.seg.ntiles, P.chunk);
-            for (uint32_t t = t0; t < t1; ++t) S::part_tile(P, sid, t, ci);
+            if (type == T_PART) {
+                for (uint32_t t = t0; t < t1; ++t) S::part_tile(P, sid, t, ci);
+            } else if (type == T_RHIST) {
+                for (uint32_t t = t0; t < t1; ++t) S::hist_tile(P, t, ci);
+            } else {
+                for (uint32_t t = t0; t < t1; ++t) S::rscat_tile(P, t, ci);
+            }
             // retire the chunk: the bulk stores complete, one gpu-scope fence per thread, one
             // counter update per CTA
             if (tid == 0) {
@@ -2251,7 +2691,12 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
             csync();
             if (sh.last) {
                 __threadfence();
-                S::finalize_part(P, sh.seg, sid);
+                if (type == T_PART)
+                    S::finalize_part(P, sh.seg, sid);
+                else if (type == T_RHIST)
+                    S::radix_hist_done(P, sh.seg, sid);
+                else
+                    S::radix_scat_done(P, sh.seg, sid);
             }
         } else {  // T_FILL
             S::fill_tile(P, sh.seg, (uint32_t)w & 0x7FFFFF);

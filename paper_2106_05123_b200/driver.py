@@ -165,6 +165,10 @@ class DeviceSorter:
                 ctypes.c_void_p(values.data_ptr() if values is not None else 0), self.n,
                 ctypes.byref(self._cfg), ctypes.c_void_p(self.workspace.data_ptr()), self.nbytes,
                 ctypes.c_void_p(s.cuda_stream))
+        if events is not None:
+            for e in events:  # torch creates the cudaEvent_t on first record: materialise it
+                if e is not None and not e.cuda_event:
+                    e.record(s)
         with torch.cuda.device(self.workspace.device):  # the C side launches on the current device
             if events is not None and len(events) == 4:
                 arr = (ctypes.c_void_p * 4)(*[e.cuda_event if e is not None else None for e in events])

@@ -178,8 +178,9 @@ def test_toggle_soundness():
 
 @pytest.mark.parametrize("dtype", DTYPES + ["kv"], ids=lambda d: d if isinstance(d, str) else np.dtype(d).name)
 def test_forced_fallback_budget_zero(dtype):
-    # bad_budget=0: the root starts with an exhausted budget, so it takes the K5 radix split
-    # (driver.py:209-213 analogue); buckets resume quicksort with a fresh budget
+    # bad_budget=0: the root starts with an exhausted budget, so it takes the K5 8-bit digit passes
+    # (driver.py:209-213 analogue: heapsort's role); the digit runs become leaves or digit passes on the
+    # next 8 bits
     rng = np.random.default_rng(5)
     for n in (30000, 300000, 1 << 22):  # above every base-case size (24572 for 4-byte keys)
         if dtype == "kv":
@@ -510,3 +511,32 @@ def test_host_sorter_kv_and_errors():
         hs.sort(np.zeros(4, np.int16))
     with pytest.raises(ValueError):
         SortConfig(block_size=0)
+
+
+@pytest.mark.parametrize("case", ["narrow", "k3", "kv_dupkeys", "kv_const_key", "f32_dups", "i64_prefix"])
+def test_forced_fallback_digit_pass_shapes(case):
+    """K5 digit passes on shapes that exercise their paths: one-digit passes skipped (shared high bits),
+    digits in the payload (equal keys, distinct payloads), runs of <= 64 sorted by warps, constant runs,
+    runs that are leaves and runs that take another digit pass; against the oracle / lexicographic order."""
+    rng = np.random.default_rng(17)
+    cfg = SortConfig(bad_budget=0)
+    for n in (70001, 1 << 20, 3 << 20):
+        vals = None
+        if case == "narrow":
+            keys = rng.integers(1 << 20, (1 << 20) + 5000, n).astype(np.int32)
+        elif case == "k3":
+            keys = rng.integers(0, 3, n).astype(np.int32)
+        elif case == "kv_dupkeys":
+            keys = rng.integers(0, 50, n).astype(np.int64)
+            vals = rng.integers(0, 2**32, n, dtype=np.uint32)
+        elif case == "kv_const_key":
+            keys = np.full(n, 7, np.int32)
+            vals = rng.integers(0, 1 << 12, n).astype(np.uint32)
+        elif case == "f32_dups":
+            keys = np.round(rng.standard_normal(n) * 100).astype(np.float32) + np.float32(0)  # no -0.0
+        else:
+            keys = (rng.integers(0, 1 << 30, n) + (1 << 40)).astype(np.int64)
+        got_k, got_v, stats = gpu_sort(keys, vals, config=cfg)
+        exp_k, exp_v = workloads.expected(keys, vals)
+        assert same_bytes(got_k, exp_k) and (vals is None or same_bytes(got_v, exp_v)), (case, n)
+        assert stats["radix_fallbacks"] >= 1 and stats["status"] == 0
