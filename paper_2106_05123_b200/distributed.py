@@ -3,23 +3,26 @@
 The reference is single-process (its sort is `driver.py:267-292` on one sequence); this is the
 scale-out the survey plans for arrays larger than one GPU's HBM or sorts spread over a node:
 
-1. every rank draws ``oversample · P`` evenly spaced samples of its shard, each sample tagged with
-   its global index (rank offset + position);
-2. one all-gather of the samples; every rank orders the same P · S samples by
-   (key, payload, global index) and picks the same P − 1 splitters at the sample quantiles;
+1. every rank draws ``oversample · P`` evenly spaced samples of its shard, each tagged with its
+   global position key ``rank << 40 | local index`` (the global index order, without exchanging
+   shard sizes first) and its shard's size;
+2. one all-gather of the samples; every rank orders the same P · S samples on the device by
+   (key, payload, position) and picks the same P − 1 splitters at the quantiles of the samples
+   weighted by their shards' sizes (a short shard counts for little);
 3. ``pdq_bucket`` (CUDA, csrc/pdq_bucket.cuh) splits the local shard into P buckets by those
-   splitters, ties broken by global index so even an all-equal input spreads evenly;
-4. an all-to-all of the bucket sizes, then one all-to-all of keys (and payload) over NCCL: rank r
-   receives bucket r of every rank;
+   splitters, ties broken by position so even an all-equal input spreads evenly;
+4. an all-to-all of the bucket sizes (the one host round trip: NCCL's all-to-all takes its split
+   sizes on the host), then one all-to-all of keys (and payload): rank r receives bucket r of every
+   rank;
 5. the received elements are sorted in place by the single-GPU sort (``sort_device``).
 
 Rank r's output is the r-th slice of the global sort; the concatenation over ranks in rank order is
 the whole array sorted.  Equal elements are bit-identical (keys) or identical pairs, so the result
 is the unique sorted array and parity with the single-GPU sort is bit-exact.
 
-Device work (bucketing, exchange, local sort) runs in CUDA and NCCL; only the splitter choice over
-the P · S gathered samples (a few thousand values) is host logic.  There is no CPU fallback: the
-bucketing and the local sort raise without the CUDA library.
+Device work (sampling, splitter choice, bucketing, exchange, local sort) runs in CUDA and NCCL;
+``choose_splitters`` is the numpy statement of the splitter rule the device code follows (tests).
+There is no CPU fallback: the bucketing and the local sort raise without the CUDA library.
 """
 
 from __future__ import annotations
@@ -34,6 +37,7 @@ from .driver import DEFAULT_CONFIG, SortConfig, _dtype_code, _raise, sort_device
 
 DEFAULT_OVERSAMPLE = 256
 MAX_RANKS = 64  # buckets per pdq_bucket call
+POS_SHIFT = 40  # global position key of an element: rank << POS_SHIFT | local index
 
 
 # ---- key images (host side of the device's Ord<U, FLOAT>, pdq_device.cuh) ----------------------
@@ -108,11 +112,16 @@ def _bucket(keys, values, gidx_base: int, splitters: np.ndarray):
     code = _dtype_code(keys.dtype)
     raw = _raw_bits(keys)
     width = keys.element_size()
-    sk_np = splitters[:, 0]
-    sk_np = sk_np.astype(np.uint32).view(np.int32) if width == 4 else sk_np
-    sk = torch.from_numpy(np.ascontiguousarray(sk_np)).to(dev).view(raw.dtype).view(keys.dtype)
-    sv = torch.from_numpy(np.ascontiguousarray(splitters[:, 1].astype(np.uint32).view(np.int32))).to(dev)
-    sg = torch.from_numpy(np.ascontiguousarray(splitters[:, 2])).to(dev)
+    if isinstance(splitters, np.ndarray):
+        splitters = torch.from_numpy(np.ascontiguousarray(splitters, dtype=np.int64)).to(dev)
+    sp = splitters.to(device=dev, dtype=torch.int64)
+    if width == 4:  # raw 32-bit patterns held in the low half of int64
+        sk = (sp[:, 0] & 0xFFFFFFFF).to(torch.int32) if sp.shape[0] else torch.empty(0, dtype=torch.int32, device=dev)
+        sk = sk.contiguous().view(keys.dtype)
+    else:
+        sk = sp[:, 0].contiguous().view(keys.dtype)
+    sv = (sp[:, 1] & 0xFFFFFFFF).to(torch.int32).contiguous()
+    sg = sp[:, 2].contiguous()
     out_k = torch.empty_like(keys)
     out_v = torch.empty_like(values) if values is not None else None
     counts = torch.zeros(nb, dtype=torch.int64, device=dev)
@@ -136,9 +145,55 @@ def _local_sort(keys, values, config: SortConfig) -> None:
         sort_device(keys, values, config)
 
 
+def sortable_i64(raw, width: int, is_float: bool):
+    """int64 tensor whose signed order is the sort's key order, for raw bit patterns given as int64
+    (4-byte keys in the low 32 bits): the device twin of ``ordered_image``."""
+    import torch
+
+    if width == 4:
+        x = raw & 0xFFFFFFFF
+        if is_float:
+            return torch.where(x >= 0x80000000, (~x) & 0xFFFFFFFF, x ^ 0x80000000)
+        return x ^ 0x80000000
+    if is_float:  # IEEE total order: negatives reversed
+        return torch.where(raw < 0, raw ^ 0x7FFFFFFFFFFFFFFF, raw)
+    return raw
+
+
+def device_splitters(rows, nranks: int, per_rank: int, width: int, is_float: bool):
+    """The P − 1 splitters (rows of (raw key bits, payload, position key), int64, on the device) from
+    the gathered sample rows (raw, payload, position, shard size; shard size 0 = padding): the rule of
+    ``choose_splitters`` with weights = shard size / the shard's sample count, computed without
+    leaving the device.  Padding rows sort last with weight 0, so they are never picked while any
+    sample is valid."""
+    import torch
+
+    if nranks <= 1:
+        return torch.empty((0, 3), dtype=torch.int64, device=rows.device)
+    valid = rows[:, 3] > 0
+    big = torch.iinfo(torch.int64).max
+    skey = torch.where(valid, sortable_i64(rows[:, 0], width, is_float), torch.full_like(rows[:, 0], big))
+    pay = torch.where(valid, rows[:, 1], torch.full_like(rows[:, 1], big))
+    pos = torch.where(valid, rows[:, 2], torch.full_like(rows[:, 2], big))
+    # weight of a sample: its shard's size over its shard's count of valid samples
+    per = valid.view(nranks, per_rank).sum(dim=1, keepdim=True).clamp(min=1)
+    w = torch.where(valid.view(nranks, per_rank), rows[:, 3].view(nranks, per_rank).double() / per.double(),
+                    torch.zeros((nranks, per_rank), dtype=torch.float64, device=rows.device)).view(-1)
+    order = torch.sort(pos, stable=True).indices
+    order = order[torch.sort(pay[order], stable=True).indices]
+    order = order[torch.sort(skey[order], stable=True).indices]
+    ws = w[order]
+    cum = torch.cumsum(ws, 0)
+    excl = cum - ws
+    tot = cum[-1]
+    targets = torch.arange(1, nranks, device=rows.device, dtype=torch.float64) * (tot / nranks) * (1 + 1e-12)
+    picks = (torch.searchsorted(excl.contiguous(), targets, right=True) - 1).clamp(min=0)
+    return rows[order[picks]][:, :3].contiguous()
+
+
 def local_samples(keys, values, base: int, count: int):
-    """``count`` rows of (raw key bits, payload, global index, valid) for one shard: evenly spaced
-    samples, padded with invalid rows when the shard is shorter than ``count``."""
+    """``count`` rows of (raw key bits, payload, global position, shard size) for one shard: evenly
+    spaced samples, padded with rows of shard size 0 when the shard is shorter than ``count``."""
     import torch
 
     dev = keys.device
@@ -196,35 +251,29 @@ def sample_sort(keys, values=None, group=None, oversample: int = DEFAULT_OVERSAM
         raise TypeError("values must be an int32/uint32 tensor of the keys' shape")
     dev = keys.device
     n_local = keys.numel()
+    if n_local >= 1 << POS_SHIFT:
+        raise ValueError(f"shards of up to 2^{POS_SHIFT} elements")
     width = keys.element_size()
     is_float = keys.dtype in (torch.float32, torch.float64)
 
-    # 1. global index base
-    sizes = torch.zeros(P, dtype=torch.int64, device=dev)
-    mine = torch.tensor([n_local], dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(sizes, mine, group=group)
-    sizes_h = sizes.cpu().tolist()
-    base = int(sum(sizes_h[:r]))
-
-    # 2. samples -> splitters (identical on every rank)
+    # 1-2. samples -> splitters on the device (identical on every rank); positions are
+    # rank << POS_SHIFT | local index, ordered like global indices without a size exchange
+    base = r << POS_SHIFT
     S = oversample * P
     smp = local_samples(keys, values, base, S)
     allsmp = torch.empty((P * S, 4), dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(allsmp, smp, group=group)
-    rows = allsmp.cpu().numpy()
-    g = valid_samples(rows)
-    splitters = choose_splitters(g, P, width, is_float, sample_weights(rows, S))
-    if splitters.shape[0] < P - 1:  # empty input everywhere: all buckets empty
-        splitters = np.zeros((P - 1, 3), dtype=np.int64)
+    splitters = device_splitters(allsmp, P, S, width, is_float)
 
     # 3. bucket the shard
     bk, bv, counts = _bucket(keys, values, base, splitters)
 
-    # 4. exchange sizes, then elements
+    # 4. exchange sizes (the one host round trip), then elements
     recv_counts = torch.empty_like(counts)
     dist.all_to_all_single(recv_counts, counts, group=group)
-    send = counts.cpu().tolist()
-    recv = recv_counts.cpu().tolist()
+    both = torch.stack([counts, recv_counts]).cpu()
+    send = both[0].tolist()
+    recv = both[1].tolist()
     total = int(sum(recv))
     out_k = torch.empty(total, dtype=keys.dtype, device=dev)
     dist.all_to_all_single(_raw_bits(out_k), _raw_bits(bk), output_split_sizes=recv, input_split_sizes=send,

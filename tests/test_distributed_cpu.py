@@ -37,6 +37,8 @@ def _key_order(t: torch.Tensor) -> np.ndarray:
 def np_bucket(keys, values, base, splitters):
     """pdq_bucket's contract (include/pdq_b200.h): bucket = #splitters below (key, payload, gidx);
     stable within a bucket."""
+    if torch.is_tensor(splitters):
+        splitters = splitters.cpu().numpy()
     n = keys.numel()
     k = _key_order(keys)
     v = values.numpy().astype(np.int64) & 0xFFFFFFFF if values is not None else np.zeros(n, np.int64)
@@ -154,6 +156,33 @@ def test_weighted_splitters_follow_shard_sizes():
     rows[:3, 3] = 300
     rows[4:8, 3] = 40
     assert list(D.sample_weights(rows, 4)) == [100.0] * 3 + [10.0] * 4
+
+
+@pytest.mark.parametrize("width,is_float", [(4, False), (4, True), (8, False), (8, True)])
+def test_device_splitters_follow_the_numpy_rule(width, is_float):
+    # device_splitters (torch, what sample_sort runs) = choose_splitters (numpy statement) with weights
+    rng = np.random.default_rng(width * 2 + is_float)
+    P, S = 4, 64
+    sizes = [5000, 0, 300, 12000]
+    blocks = []
+    for r in range(P):
+        m = min(S, sizes[r])
+        if width == 4:
+            raw = (rng.standard_normal(m).astype(np.float32).view(np.uint32).astype(np.int64) if is_float
+                   else rng.integers(0, 2**32, m).astype(np.int64))
+        else:
+            raw = rng.standard_normal(m).view(np.int64) if is_float else rng.integers(-2**63, 2**63, m)
+        raw[: m // 3] = raw[0] if m else raw[: m // 3]  # duplicate keys: ties by payload, then position
+        rows = np.zeros((S, 4), np.int64)
+        rows[:m, 0] = raw
+        rows[:m, 1] = rng.integers(0, 3, m)
+        rows[:m, 2] = (r << D.POS_SHIFT) + np.arange(m)
+        rows[:m, 3] = sizes[r]
+        blocks.append(rows)
+    rows = np.concatenate(blocks)
+    dev = D.device_splitters(torch.from_numpy(rows), P, S, width, is_float).numpy()
+    ref = D.choose_splitters(D.valid_samples(rows), P, width, is_float, D.sample_weights(rows, S))
+    assert dev.shape == (P - 1, 3) and (dev == ref).all()
 
 
 def test_ordered_image_matches_numeric_order():
