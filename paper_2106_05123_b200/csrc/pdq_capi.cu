@@ -108,7 +108,7 @@ Layout layout(int dtype, int has_payload, int64_t n) {
     off += a256((size_t)L.leaf_cap * 8);
     // K5 digit passes: one slot of RDIG 64-bit counters per radix segment (bump-allocated; when they
     // run out a segment falls back to one-bit radix exchange, which needs none)
-    L.rslot_cap = (uint32_t)((uint64_t)n / 8192 + 512);
+    L.rslot_cap = (uint32_t)((uint64_t)n / 32768 + 512);
     L.rslots = off;
     off += a256((size_t)L.rslot_cap * RDIG * 8);
     L.total = off;
