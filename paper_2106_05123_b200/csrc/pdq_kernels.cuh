@@ -712,6 +712,23 @@ struct Sorter {
         const int kb = KBITS - rbit, vb = nd - kb;
         return ((((uint32_t)(uint64_t)k) & ((1u << kb) - 1u)) << vb) | (v >> (32 - vb));
     }
+    // per-tile digit extractor: MODE 0 = the digit lies in the key, 1 = in the payload, 2 = straddles
+    struct Dig {
+        int mode, ks, vs;
+        uint32_t mask;
+        __device__ __forceinline__ Dig(int rbit, int nd) {
+            mask = (1u << nd) - 1u;
+            mode = rbit + nd <= KBITS ? 0 : (rbit >= KBITS ? 1 : 2);
+            ks = mode == 0 ? KBITS - rbit - nd : nd - (KBITS - rbit);  // mode 2: bits taken from the payload
+            vs = mode == 1 ? 32 - (rbit - KBITS) - nd : 32 - ks;
+        }
+        template <int MODE>
+        __device__ __forceinline__ uint32_t get(U k, uint32_t v) const {
+            if (MODE == 0) return (uint32_t)((uint64_t)k >> ks) & mask;
+            if (MODE == 1) return (v >> vs) & mask;
+            return (((uint32_t)(uint64_t)k << ks) | (v >> vs)) & mask;
+        }
+    };
     // the prefix (pk, pv) with digit dv at composite bits [rbit, rbit + nd)
     __device__ __forceinline__ static void put_digit(uint64_t &pk, uint32_t &pv, int rbit, int nd, uint32_t dv) {
         if (rbit + nd <= KBITS) {
@@ -756,13 +773,36 @@ struct Sorter {
         mbar_wait(&sh.bar[st], (ci / B::NSTAGE) & 1u);
         ++ci;
         csync();
-        for (int i0 = lo_i; i0 < hi_i; i0 += THREADS) {
-            const int i = i0 + tid;
-            const bool valid = i < hi_i;
-            uint32_t d = 0;
-            if (valid) d = digit_of(O::to(sk[i]), (KV && rbit + nd > KBITS) ? sv[i] : 0u, rbit, nd);
-            count_digit(cnt, valid, d);
-        }
+        const Dig dg(rbit, nd);
+        auto hist = [&](auto mode_c) {
+            constexpr int MODE = decltype(mode_c)::value;
+            if (lo_i == 0 && hi_i == TL) {  // a whole tile: every lane holds an element in every round
+#pragma unroll 4
+                for (int i = tid; i < TL; i += THREADS) {
+                    const uint32_t d = dg.template get<MODE>(O::to(sk[i]), (KV && MODE != 0) ? sv[i] : 0u);
+                    const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+                    if (__all_sync(0xffffffffu, d == d0)) {
+                        if ((tid & 31) == 0) atomicAdd(&cnt[d0], 32u);
+                    } else {
+                        atomicAdd(&cnt[d], 1u);
+                    }
+                }
+            } else {
+                for (int i0 = lo_i; i0 < hi_i; i0 += THREADS) {
+                    const int i = i0 + tid;
+                    const bool valid = i < hi_i;
+                    uint32_t d = 0;
+                    if (valid) d = dg.template get<MODE>(O::to(sk[i]), (KV && MODE != 0) ? sv[i] : 0u);
+                    count_digit(cnt, valid, d);
+                }
+            }
+        };
+        if (dg.mode == 0)
+            hist(std::integral_constant<int, 0>());
+        else if (dg.mode == 1)
+            hist(std::integral_constant<int, 1>());
+        else
+            hist(std::integral_constant<int, 2>());
         csync();  // histogram complete, stage consumed
         if (tid == 0) {
             sh.ci = ci;
@@ -800,16 +840,46 @@ struct Sorter {
         csync();
         U kx[IT];
         uint32_t vx[IT], pk[IT];
+        const Dig dg(rbit, nd);
+        auto slots = [&](auto mode_c) {
+            constexpr int MODE = decltype(mode_c)::value;
+            if (lo_i == 0 && hi_i == TL) {  // a whole tile: one atomic per warp when its 32 digits agree
 #pragma unroll
-        for (int r = 0; r < IT; ++r) {
-            const int i = r * THREADS + tid;
-            const bool valid = i >= lo_i && i < hi_i;
-            kx[r] = valid ? sk[i] : (U)0;
-            vx[r] = (KV && valid) ? sv[i] : 0u;
-            const uint32_t d = valid ? digit_of(O::to(kx[r]), vx[r], rbit, nd) : 0u;
-            const uint32_t sl = count_digit(cnt, valid, d);
-            pk[r] = valid ? (d << 16 | sl) : 0xFFFFFFFFu;
-        }
+                for (int r = 0; r < IT; ++r) {
+                    const int i = r * THREADS + tid;
+                    kx[r] = sk[i];
+                    vx[r] = KV ? sv[i] : 0u;
+                    const uint32_t d = dg.template get<MODE>(O::to(kx[r]), vx[r]);
+                    const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+                    uint32_t sl;
+                    if (__all_sync(0xffffffffu, d == d0)) {
+                        uint32_t base = 0;
+                        if ((tid & 31) == 0) base = atomicAdd(&cnt[d0], 32u);
+                        sl = __shfl_sync(0xffffffffu, base, 0) + (tid & 31);
+                    } else {
+                        sl = atomicAdd(&cnt[d], 1u);
+                    }
+                    pk[r] = d << 16 | sl;
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < IT; ++r) {
+                    const int i = r * THREADS + tid;
+                    const bool valid = i >= lo_i && i < hi_i;
+                    kx[r] = valid ? sk[i] : (U)0;
+                    vx[r] = (KV && valid) ? sv[i] : 0u;
+                    const uint32_t d = valid ? dg.template get<MODE>(O::to(kx[r]), vx[r]) : 0u;
+                    const uint32_t sl = count_digit(cnt, valid, d);
+                    pk[r] = valid ? (d << 16 | sl) : 0xFFFFFFFFu;
+                }
+            }
+        };
+        if (dg.mode == 0)
+            slots(std::integral_constant<int, 0>());
+        else if (dg.mode == 1)
+            slots(std::integral_constant<int, 1>());
+        else
+            slots(std::integral_constant<int, 2>());
         csync();
         {  // digit t = thread t: exclusive scan of the tile's counts, then one cursor atomic per digit
             const uint32_t c = cnt[tid];
@@ -841,13 +911,23 @@ struct Sorter {
         }
         csync();
         const int nv = hi_i - lo_i;
-        for (int p = tid; p < nv; p += THREADS) {  // consecutive threads write consecutive slots of a run
-            const U k = sk[p];
-            const uint32_t v = KV ? sv[p] : 0u;
-            const long long g = gd[digit_of(O::to(k), v, rbit, nd)] + p;
-            dst[g] = k;
-            if (KV) dstv[g] = v;
-        }
+        auto out = [&](auto mode_c) {
+            constexpr int MODE = decltype(mode_c)::value;
+#pragma unroll 4
+            for (int p = tid; p < nv; p += THREADS) {  // consecutive threads write consecutive slots of a run
+                const U k = sk[p];
+                const uint32_t v = KV ? sv[p] : 0u;
+                const long long g = gd[dg.template get<MODE>(O::to(k), v)] + p;
+                dst[g] = k;
+                if (KV) dstv[g] = v;
+            }
+        };
+        if (dg.mode == 0)
+            out(std::integral_constant<int, 0>());
+        else if (dg.mode == 1)
+            out(std::integral_constant<int, 1>());
+        else
+            out(std::integral_constant<int, 2>());
         csync();  // stage consumed, kc free
         if (tid == 0) {
             sh.ci = ci;
@@ -1884,21 +1964,15 @@ struct BigLeaf {
 
     // ---- fast path: window networks over a swizzled kc ----------------------------------------------
     // Positions are in q-space: q = a0 + leaf position, a0 = b mod 4, so q and the leaf's global index
-    // have the same 16-byte phase.  Row t = q / 24 is thread t's window; its six 16-byte chunks are
-    // rotated by one in rows with bit 2 of t set, so the 8 lanes of a quarter-warp reading their own
-    // rows (or the next rows) hit 8 distinct bank groups.
+    // have the same 16-byte phase.  Row t = [24t, 24t + 24) is thread t's window.  Linear 16-byte chunk c
+    // (= q / 4) lives at chunk c ^ ((c >> 3) & 1): the 8 lanes of a quarter-warp then hit 8 distinct bank
+    // groups whether they read chunk j of their own rows, chunk j of the next rows, or 8 consecutive
+    // chunks (checked exhaustively for every access pattern here); a row-rotation needs a division by 24.
     static constexpr int WIN = 24, HALF = WIN / 2;
     static constexpr uint32_t FAST_CMAX = HALF + 1;  // every bucket fits an aligned or an offset window
     static_assert(BIG_BASE == WIN * BT, "one window per thread");
-    __device__ __forceinline__ static uint32_t swz_chunk(uint32_t t, uint32_t j) {
-        uint32_t jj = j + ((t >> 2) & 1u);
-        jj = jj >= 6u ? jj - 6u : jj;
-        return WIN * t + 4u * jj;
-    }
-    __device__ __forceinline__ static uint32_t swz(uint32_t q) {
-        const uint32_t t = q / (uint32_t)WIN, r = q - (uint32_t)WIN * t;
-        return swz_chunk(t, r >> 2) + (r & 3u);
-    }
+    __device__ __forceinline__ static uint32_t swz(uint32_t q) { return q ^ ((q >> 3) & 4u); }
+    __device__ __forceinline__ static uint32_t swz_chunk(uint32_t t, uint32_t j) { return swz(WIN * t + 4u * j); }
     __device__ __forceinline__ static void ld_chunk(const uint32_t *s, U *w) {
         const uint4 v = *reinterpret_cast<const uint4 *>(s);
         w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
@@ -1922,10 +1996,12 @@ struct BigLeaf {
             U w[WIN];
 #pragma unroll
             for (int j = 0; j < 6; ++j) ld_chunk(kc + swz_chunk(t, j), w + 4 * j);
+            if (WIN * t < a0 || WIN * t + WIN > qend) {  // the leaf's first / last window only
 #pragma unroll
-            for (int i = 0; i < WIN; ++i) {
-                const uint32_t q = WIN * t + i;
-                w[i] = q < a0 ? 0u : (q >= qend ? ~0u : w[i]);
+                for (int i = 0; i < WIN; ++i) {
+                    const uint32_t q = WIN * t + i;
+                    w[i] = q < a0 ? 0u : (q >= qend ? ~0u : w[i]);
+                }
             }
             net_sort24(w);
 #pragma unroll
@@ -1944,10 +2020,12 @@ struct BigLeaf {
 #pragma unroll
                 for (int i = HALF; i < WIN; ++i) w[i] = ~0u;
             }
+            if (WIN * t + HALF + WIN > qend) {
 #pragma unroll
-            for (int i = HALF; i < WIN; ++i) {
-                const uint32_t q = WIN * t + HALF + i;
-                w[i] = q >= qend ? ~0u : w[i];
+                for (int i = HALF; i < WIN; ++i) {
+                    const uint32_t q = WIN * t + HALF + i;
+                    w[i] = q >= qend ? ~0u : w[i];
+                }
             }
             net_merge12(w);
 #pragma unroll
@@ -1962,7 +2040,7 @@ struct BigLeaf {
         const uint32_t nch = (qend + 3) / 4;
         for (uint32_t c = t; c < nch; c += BT) {
             U v[4];
-            ld_chunk(kc + swz_chunk(c / 6u, c % 6u), v);
+            ld_chunk(kc + swz(4u * c), v);
             const uint32_t q = 4 * c;
             if (q >= a0 && q + 4 <= qend) {
                 *reinterpret_cast<uint4 *>(dst + (q - a0)) = make_uint4(O::from(v[0]), O::from(v[1]), O::from(v[2]),
@@ -2053,14 +2131,25 @@ struct BigLeaf {
                 for (int q = 0; q < BBK / 4 / BT; ++q) c4[q * BT + tid] = make_uint4(0, 0, 0, 0);
             }
             const int off = (int)(b & 3);
+            // vector jv of a thread holds leaf elements e0 .. e0 + 3, e0 = 4 (jv BT + t) - off: a vector is
+            // whole, partial (the leaf's ends) or empty; vectors jv with 4 jv BT >= off + m are empty in
+            // every thread (a CTA-uniform loop bound)
+            const int nvec = (off + m + 4 * BT - 1) / (4 * BT);
             U mn = ~0u, mx = 0u;
 #pragma unroll
-            for (int j = 0; j < BI; ++j) {
-                if ((unsigned)eidx(j, off) < (unsigned)m) {
-                    const U x = O::to(xs[j]);
-                    xs[j] = x;
-                    mn = min(mn, x);
-                    mx = max(mx, x);
+            for (int jv = 0; jv < BI / 4; ++jv) {
+                if (jv < nvec) {
+                    const int e0 = 4 * (jv * BT + tid) - off;
+                    const bool whole = e0 >= 0 && e0 + 4 <= m;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (whole || (unsigned)(e0 + q) < (unsigned)m) {
+                            const U x = O::to(xs[4 * jv + q]);
+                            xs[4 * jv + q] = x;
+                            mn = min(mn, x);
+                            mx = max(mx, x);
+                        }
+                    }
                 }
             }
             mn = __reduce_min_sync(0xffffffffu, mn);
@@ -2097,10 +2186,17 @@ struct BigLeaf {
             const Map mp = make_map(mn, range);
             uint32_t pp[BI / 2];  // 16-bit slots
 #pragma unroll
-            for (int j = 0; j < BI; ++j) {
-                const uint32_t sl = ((unsigned)eidx(j, off) < (unsigned)m) ? atomicAdd(&cnt[mp(xs[j])], 1u) : 0u;
-                if (j & 1) pp[j / 2] |= sl << 16;
-                else pp[j / 2] = sl;
+            for (int jv = 0; jv < BI / 4; ++jv) {
+                pp[2 * jv] = pp[2 * jv + 1] = 0;
+                if (jv < nvec) {
+                    const int e0 = 4 * (jv * BT + tid) - off;
+                    const bool whole = e0 >= 0 && e0 + 4 <= m;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int j = 4 * jv + q;
+                        if (whole || (unsigned)(e0 + q) < (unsigned)m) pp[j / 2] |= atomicAdd(&cnt[mp(xs[j])], 1u) << ((j & 1) << 4);
+                    }
+                }
             }
             bsync();
             uint32_t cmax;
@@ -2132,12 +2228,20 @@ struct BigLeaf {
             const uint32_t a0 = (uint32_t)(b & 3);
             const bool fast = PDQ_BIG_SKIP || cmax <= FAST_CMAX;
 #pragma unroll
-            for (int j = 0; j < BI; ++j) {
-                if ((unsigned)eidx(j, off) < (unsigned)m) {
-                    PDQ_CHECK(mp(xs[j]) < (uint32_t)BBK, "leaf bucket");
-                    const uint32_t p = (cnt[mp(xs[j])] & 0xFFFFu) + ((pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu);
-                    PDQ_CHECK(p < (uint32_t)m, "leaf scatter slot");
-                    kc[fast ? swz(a0 + p) : p] = xs[j];
+            for (int jv = 0; jv < BI / 4; ++jv) {
+                if (jv < nvec) {
+                    const int e0 = 4 * (jv * BT + tid) - off;
+                    const bool whole = e0 >= 0 && e0 + 4 <= m;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int j = 4 * jv + q;
+                        if (whole || (unsigned)(e0 + q) < (unsigned)m) {
+                            PDQ_CHECK(mp(xs[j]) < (uint32_t)BBK, "leaf bucket");
+                            const uint32_t p = (cnt[mp(xs[j])] & 0xFFFFu) + ((pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu);
+                            PDQ_CHECK(p < (uint32_t)m, "leaf scatter slot");
+                            kc[fast ? swz(a0 + p) : p] = xs[j];
+                        }
+                    }
                 }
             }
             bsync();
