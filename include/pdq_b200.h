@@ -94,6 +94,8 @@ typedef struct pdq_stats {
     int64_t sched_fetch;            /*   ... polling the ring, copying descriptors, issuing loads */
     int64_t sched_idle;             /*   ... sleeping with nothing to do */
     int64_t bytes_base;             /* algorithmic bytes of the K7 base-case kernel (not in bytes_algorithmic) */
+    int64_t sort_ns;                /* device-timer span of the persistent sorter (first CTA start -> last end) */
+    int64_t base_ns;                /*   ... of the base-case kernel (0 if it did not run) */
 } pdq_stats;
 
 /* Fill `cfg` with the reference defaults (driver.py:55-63) and GPU defaults. */

@@ -90,6 +90,8 @@ STAT_FIELDS = (
     "sched_fetch",
     "sched_idle",
     "bytes_base",
+    "sort_ns",
+    "base_ns",
 )
 
 

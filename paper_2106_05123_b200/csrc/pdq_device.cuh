@@ -49,7 +49,7 @@ enum : uint32_t {
     I_COUNT_EQ = 1u << 4, // the sample's low end repeats the pivot: count keys equal to it
     I_RADIX = 1u << 5,    // K5 fallback: radix exchange on composite bit `rbit` (threshold pivot)
     I_HAS_UB = 1u << 6,   // `ub` is a valid exclusive upper bound
-    I_RADIX8 = 1u << 7,   // K5 fallback: 8-bit digit pass on composite bits [rbit, rbit + 8) (slot `rslot`)
+    I_RADIX8 = 1u << 7,   // K5 fallback: digit pass on composite bits [rbit, rbit + pivot_v) (slot `rslot`)
 };
 constexpr int RDIG = 256;  // digits of a K5 radix pass
 
@@ -95,6 +95,10 @@ struct __align__(128) State {
         c_bytes, c_bytes_check, c_bytes_base;
     unsigned long long c_cyc_wait, c_cyc_work, c_cyc_base, c_cyc_spawn;  // SM cycles by phase (thread 0)
     unsigned long long c_sch_retire, c_sch_claim, c_sch_fetch, c_sch_idle;  // scheduler-thread cycles
+    // device-timer spans (%globaltimer ns) of the two big kernels, first CTA start (stored inverted, so
+    // a zeroed state and atomicMax give the minimum) to last CTA end: per-kernel times without events
+    // between the kernels (which would end their programmatic overlap)
+    unsigned long long t_sort_b_inv, t_sort_e, t_base_b_inv, t_base_e;
 };
 
 struct Params {

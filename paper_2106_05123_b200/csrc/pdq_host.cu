@@ -332,8 +332,8 @@ extern "C" int pdq_host_sort(pdq_host_sorter *h, void *keys, int dtype, uint32_t
     const auto t1 = std::chrono::steady_clock::now();
 
     // 2. sort (stream-ordered), then the status: nothing is copied back from a failed sort
-    rc = pdq_sort_ex(h->d_keys, dtype, payload ? (uint32_t *)h->d_vals : nullptr, n, cfg, h->d_ws, h->cap_ws,
-                     h->stream, h->ev_k0, h->ev_k1);
+    rc = pdq_sort(h->d_keys, dtype, payload ? (uint32_t *)h->d_vals : nullptr, n, cfg, h->d_ws, h->cap_ws,
+                  h->stream);
     if (rc) return rc;
     if ((e = cudaEventRecord(h->ev_sort, h->stream)) != cudaSuccess) return fail(h, "event", e);
     rc = pdq_sort_finish(h->d_ws, stats, h->stream);  // synchronises the sort stream

@@ -37,7 +37,13 @@ __device__ __forceinline__ uint32_t task_end_tile(uint32_t first, uint32_t N, ui
 #ifndef PDQ_NST
 #define PDQ_NST 1
 #endif
-constexpr int NST = PDQ_NST;            // TMA stages: tile loads run up to NST tiles ahead of compute
+constexpr int NST = PDQ_NST;
+#ifndef PDQ_SLEEP_CAP
+#define PDQ_SLEEP_CAP 256  // ns: the longest back-off of a CTA polling the ring for its next task
+#endif
+#ifndef PDQ_PAIR
+#define PDQ_PAIR 1  // spawn both children of a partition with one ring reservation (spawn_pair)
+#endif            // TMA stages: tile loads run up to NST tiles ahead of compute
 // CTA barrier (named barrier 1, all THREADS threads)
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(THREADS) : "memory"); }
 __device__ __forceinline__ int csync_or(int p) {
@@ -70,7 +76,7 @@ struct Shared {
     Seg nseg;
     unsigned long long npos; // ring position claimed for the next task
     uint64_t lf[2];          // K7: descriptors of the current and the next leaf
-    uint64_t lq[3];          // K7 (k_base_big): current, next and claimed-after-next leaf descriptors
+    uint64_t lq[2];          // K7 (k_base_big): current and next leaf descriptors
     long long lc0;           // K7: cycle stamp of the current leaf (counters)
     int nstate;              // 0 none, 1 claimed (unpublished), 2 ready, 3 exit
     // load cursor (thread 0): tiles issued so far, and which task/tile is the next to load
@@ -99,6 +105,11 @@ struct Shared {
 // (inlined or not) addresses them as shared memory (LDS/STS, never generic LD/ST).
 __shared__ Shared g_sh;
 extern __shared__ __align__(128) unsigned char g_dsm[];
+
+// programmatic dependent launch (launch_pdl in pdq_capi.cu): wait for the stream's previous kernel /
+// let the next kernel of the stream be scheduled
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t mix32(uint64_t x) {
     x ^= x >> 33;
@@ -514,9 +525,37 @@ struct Sorter {
             }
             return radix8_start(P, b, e, srcB, bit, pk, pv, depth, reuse_sid);
         }
-        // K1: stratified samples (64, or SAMPLES for segments of 2^20+ keys); perturbed strata
-        // after a bad partition.  The median of the sorted sample is the pivot.
+        // K1: stratified samples (64, or SAMPLES for segments of 2^20+ keys) sorted by warp 0; perturbed
+        // strata after a bad partition.  The median of the sorted sample is the pivot.
         const long long c0 = clock64();
+        if (tid < 32) warp_sample(P, b, m, srcB, perturb, depth, 0);
+        csync();
+        const uint32_t ntiles = (uint32_t)((e - 1) / TL - b / TL + 1);
+        if (tid == 0) {
+            const uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
+            sh.new_sid = sid;
+            if (sid >= P.seg_cap) {
+                fail(P, -6);
+            } else {
+                write_part_seg(P, sid, b, e, srcB, bd, budget, depth, perturb, 0);
+                __threadfence();
+                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)seg_ntasks(ntiles, P.chunk));
+            }
+        }
+        csync();
+        if (sh.new_sid < P.seg_cap) push_tasks(P, T_PART, sh.new_sid, ntiles);
+        csync();
+        if (tid == 0) sh.s_cyc_spawn += clock64() - c0;
+        return reuse_sid >= 0;
+    }
+
+    // One warp: stratified samples of [b, b + m) (64, or SAMPLES = 256 for 2^20+ keys; perturbed strata
+    // after a bad partition, break_patterns' role) sorted in registers by a warp bitonic network; the
+    // median goes to sample slot `slot` (samp_k/samp_v[2 slot]), the smallest sample to samp_k[2 slot + 1].
+    __device__ static void warp_sample(const Params &P, int64_t b, int64_t m, bool srcB, bool perturb, int depth,
+                                       int slot) {
+        Shared &sh = g_sh;
+        const int lane = threadIdx.x & 31;
         const U *src = (const U *)(srcB ? P.b_keys : P.a_keys);
         const uint32_t *srcv = srcB ? P.b_vals : P.a_vals;
         const int ns = m >= (1 << 20) ? SAMPLES : 64;
@@ -528,80 +567,102 @@ struct Sorter {
                        ns;
             return ((int64_t)(2 * i + 1) * m) / (2 * ns);
         };
-        uint64_t piv, lo_sample;
-        uint32_t pv;
-        if (ns == 64) {
-            if (tid < 32) {
-                uint64_t x[2];
-                uint32_t y[2];
+        auto run = [&](auto pl_c) {
+            constexpr int PL = decltype(pl_c)::value;
+            uint64_t x[PL];
+            uint32_t y[PL];
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int64_t off = sample_at(2 * tid + q);
-                    x[q] = (uint64_t)O::to(ldcg(src + b + off));
-                    y[q] = KV ? ldcg(srcv + b + off) : 0u;
-                }
-                warp_bitonic<2>(x, y);
-                if (tid == 16) {  // element 32 = lane 16, slot 0
-                    B::samp_k()[0] = x[0];
-                    B::samp_v()[0] = y[0];
-                }
-                if (tid == 0) B::samp_k()[1] = x[0];  // the smallest sample
+            for (int q = 0; q < PL; ++q) {
+                const int64_t off = sample_at(PL * lane + q);
+                x[q] = (uint64_t)O::to(ldcg(src + b + off));
+                y[q] = KV ? ldcg(srcv + b + off) : 0u;
             }
-            csync();
-            piv = B::samp_k()[0];
-            pv = B::samp_v()[0];
-            lo_sample = B::samp_k()[1];
-        } else {
-            for (int i = tid; i < SAMPLES; i += THREADS) {
-                const int64_t off = sample_at(i);
-                B::samp_k()[i] = (uint64_t)O::to(ldcg(src + b + off));
-                B::samp_v()[i] = KV ? ldcg(srcv + b + off) : 0;
+            warp_bitonic<PL>(x, y);
+            if (lane == 16) {  // element 16 PL (the median) = lane 16, register 0
+                B::samp_k()[2 * slot] = x[0];
+                B::samp_v()[2 * slot] = y[0];
             }
-            csync();
-            bitonic_samples(B::samp_k(), B::samp_v(), SAMPLES);
-            piv = B::samp_k()[SAMPLES / 2];
-            pv = B::samp_v()[SAMPLES / 2];
-            lo_sample = B::samp_k()[0];
-        }
+            if (lane == 0) B::samp_k()[2 * slot + 1] = x[0];  // the smallest sample
+        };
+        if (ns == 64)
+            run(std::integral_constant<int, 2>());
+        else
+            run(std::integral_constant<int, SAMPLES / 32>());
+        if (lane == 0) atomicAdd(&sh.s_bytes, (unsigned long long)ns * ELEM_BYTES);
+    }
+
+    // thread 0: the descriptor of partition segment [b, e) (buffer srcB) with the pivot of sample slot
+    // `slot`: partition_left when the predecessor equals the pivot (driver.py:222), equal counting when
+    // the sample's low end repeats the pivot
+    __device__ static void write_part_seg(const Params &P, uint32_t sid, int64_t b, int64_t e, bool srcB,
+                                          const Bnd &bd, int budget, int depth, bool perturb, int slot) {
+        const uint64_t piv = B::samp_k()[2 * slot], lo_sample = B::samp_k()[2 * slot + 1];
+        const uint32_t pv = B::samp_v()[2 * slot];
         const bool dup_heavy = lo_sample == piv;  // the low end of the sample repeats the pivot
-        // driver.py:222: a predecessor not less than the pivot equals it -> partition_left
-        const bool left = P.use_left && has_lb && !pless<KV>(lb, lbv, piv, pv);
-        const uint32_t ntiles = (uint32_t)((e - 1) / TL - b / TL + 1);
+        const bool left = P.use_left && bd.has_lb && !pless<KV>(bd.lb, bd.lbv, piv, pv);
+        Seg *s = &P.segs[sid];
+        s->begin = b;
+        s->end = e;
+        s->pivot = (uint64_t)O::from((U)piv);  // raw bits: tiles compare raw keys
+        s->pivot_v = pv;
+        s->lb = bd.lb;
+        s->lb_v = bd.lbv;
+        s->ntiles = (uint32_t)((e - 1) / TL - b / TL + 1);
+        s->info = (srcB ? I_SRC_B : 0) | (left ? I_LEFT : 0) | (bd.has_lb ? I_HAS_LB : 0) |
+                  (bd.has_ub ? I_HAS_UB : 0) | (perturb ? I_PERTURB : 0) | (dup_heavy ? I_COUNT_EQ : 0);
+        s->budget = budget > 0 ? budget : 0;
+        s->depth = depth;
+        s->ub = bd.ub;
+        s->ub_v = bd.ubv;
+        s->cnt_left = 0;
+        s->cnt_right = 0;
+        s->cnt_eq = 0;
+        s->tiles_done = 0;
+    }
+
+    // Both children of a partition are big partition segments: warps 0 and 1 sample them at once and
+    // one ring reservation publishes both (halves the finalize -> first-tile latency of a tree level).
+    // Returns false (nothing done) when the pair does not qualify; spawn() then handles each child.
+    __device__ static bool spawn_pair(const Params &P, int64_t b, int64_t mid, int64_t e, bool srcB,
+                                      const Bnd &lbd, const Bnd &rbd, int budget, int depth, bool perturb,
+                                      int reuse_sid) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x, warp = tid >> 5;
+        if (!PDQ_PAIR || budget <= 0 || P.debug_depth || mid - b <= P.base_size || e - mid <= P.base_size ||
+            reuse_sid < 0)
+            return false;
+        const long long c0 = clock64();
+        if (warp < 2) warp_sample(P, warp ? mid : b, warp ? e - mid : mid - b, srcB, perturb, depth, warp);
+        csync();
+        const uint32_t ntL = (uint32_t)((mid - 1) / TL - b / TL + 1), ntR = (uint32_t)((e - 1) / TL - mid / TL + 1);
+        const uint32_t nkL = seg_ntasks(ntL, P.chunk), nkR = seg_ntasks(ntR, P.chunk);
         if (tid == 0) {
-            uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
-            sh.new_sid = sid;
-            sh.s_bytes += (unsigned long long)SAMPLES * ELEM_BYTES;
-            if (sid >= P.seg_cap) {
+            const uint32_t sidL = (uint32_t)reuse_sid, sidR = atomicAdd(&P.st->seg_alloc, 1u);
+            sh.new_sid = sidR;
+            if (sidR >= P.seg_cap) {
                 fail(P, -6);
             } else {
-                Seg *s = &P.segs[sid];
-                s->begin = b;
-                s->end = e;
-                s->pivot = (uint64_t)O::from((U)piv);  // raw bits: tiles compare raw keys
-                s->pivot_v = pv;
-                s->lb = lb;
-                s->lb_v = lbv;
-                s->ntiles = ntiles;
-                s->info = (srcB ? I_SRC_B : 0) | (left ? I_LEFT : 0) | (has_lb ? I_HAS_LB : 0) |
-                          (bd.has_ub ? I_HAS_UB : 0) |
-                          (perturb ? I_PERTURB : 0) | (dup_heavy ? I_COUNT_EQ : 0);
-                s->budget = budget > 0 ? budget : 0;
-                s->depth = depth;
-                s->ub = bd.ub;
-                s->ub_v = bd.ubv;
-                s->cnt_left = 0;
-                s->cnt_right = 0;
-                s->cnt_eq = 0;
-                s->tiles_done = 0;
+                write_part_seg(P, sidL, b, mid, srcB, lbd, budget, depth, perturb, 0);
+                write_part_seg(P, sidR, mid, e, srcB, rbd, budget, depth, perturb, 1);
                 __threadfence();
-                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)seg_ntasks(ntiles, P.chunk));
+                sh.push_pos = atomicAdd(&P.st->q_tail, (unsigned long long)(nkL + nkR));
+            }
+            if (depth > sh.s_max_depth) sh.s_max_depth = depth;
+        }
+        csync();
+        if (sh.new_sid < P.seg_cap) {
+            const unsigned long long pos = sh.push_pos;
+            const uint64_t mask = (1ull << P.log_q) - 1;
+            for (uint32_t t = tid; t < nkL + nkR; t += THREADS) {
+                const bool r = t >= nkL;
+                const uint32_t k = r ? t - nkL : t;
+                *(volatile uint64_t *)&P.ring[(pos + t) & mask] =
+                    task_word(pos + t, P.log_q, T_PART, r ? sh.new_sid : (uint32_t)reuse_sid, k * P.chunk);
             }
         }
         csync();
-        if (sh.new_sid < P.seg_cap) push_tasks(P, T_PART, sh.new_sid, ntiles);
-        csync();
         if (tid == 0) sh.s_cyc_spawn += clock64() - c0;
-        return reuse_sid >= 0;
+        return true;
     }
 
     // ---- K5 + K6: the last tile of a segment decides its children ----------------------------
@@ -658,8 +719,10 @@ struct Sorter {
             rbd.has_lb = true;
             rbd.lb = piv_ord;
             rbd.lbv = sg.pivot_v;
-            bool used = spawn(P, b, b + L, dstB, lbd, nb, sg.depth + 1, perturb, (int)sid);
-            spawn(P, b + L, e, dstB, rbd, nb, sg.depth + 1, perturb, used ? -1 : (int)sid);
+            if (!spawn_pair(P, b, b + L, e, dstB, lbd, rbd, nb, sg.depth + 1, perturb, (int)sid)) {
+                bool used = spawn(P, b, b + L, dstB, lbd, nb, sg.depth + 1, perturb, (int)sid);
+                spawn(P, b + L, e, dstB, rbd, nb, sg.depth + 1, perturb, used ? -1 : (int)sid);
+            }
         } else {
             if (tid == 0) sh.s_part_left++;
             bool used = false;
@@ -701,9 +764,18 @@ struct Sorter {
     // digit's cursor, and writes its runs to the other buffer.  The 256 children then become leaves or
     // radix segments on the next 8 bits -- the work is bounded by the key width, never quadratic.  A pass
     // whose histogram finds a single digit skips the scatter.  (Bits are MSB-first composite positions.)
-    __device__ __forceinline__ static int rdigits(int rbit) { return NBITS - rbit < 8 ? NBITS - rbit : 8; }
+    // Digit width of a pass over m elements: 8 bits, or fewer when 256 runs would be much smaller than a
+    // leaf (a uniform segment then splits into runs of about half the base-case size instead of many tiny
+    // leaves); never past the composite's last bit.  Stored in the segment (Seg::pivot_v).
+    __device__ __forceinline__ static int rwidth(const Params &P, int64_t m, int rbit) {
+        const int64_t target = P.base_size / 2 > 64 ? P.base_size / 2 : 64;
+        int nd = 1;
+        while (nd < 8 && (m >> nd) > target) ++nd;
+        return nd < NBITS - rbit ? nd : NBITS - rbit;
+    }
+    __device__ __forceinline__ static int rdigits(const Seg &sg) { return (int)sg.pivot_v; }
     __device__ __forceinline__ static bool hist_keys_only(uint64_t task, const Seg &sg) {
-        return ((uint32_t)(task >> 45) & 7u) == T_RHIST && (int)sg.rbit + rdigits((int)sg.rbit) <= KBITS;
+        return ((uint32_t)(task >> 45) & 7u) == T_RHIST && (int)sg.rbit + rdigits(sg) <= KBITS;
     }
     __device__ __forceinline__ static uint32_t digit_of(U k, uint32_t v, int rbit, int nd) {
         const uint32_t mask = (1u << nd) - 1u;
@@ -767,7 +839,7 @@ struct Sorter {
         const int st = (int)(ci % B::NSTAGE);
         const U *sk = B::stage(st);
         const uint32_t *sv = KV ? B::vstage(st) : nullptr;
-        const int rbit = (int)sg.rbit, nd = rdigits(rbit);
+        const int rbit = (int)sg.rbit, nd = rdigits(sg);
         uint32_t *cnt = reinterpret_cast<uint32_t *>(B::kc());
         cnt[tid] = 0;  // THREADS == RDIG
         mbar_wait(&sh.bar[st], (ci / B::NSTAGE) & 1u);
@@ -826,7 +898,7 @@ struct Sorter {
         const int st = (int)(ci % B::NSTAGE);
         U *sk = B::stage(st);
         uint32_t *sv = KV ? B::vstage(st) : nullptr;
-        const int rbit = (int)sg.rbit, nd = rdigits(rbit);
+        const int rbit = (int)sg.rbit, nd = rdigits(sg);
         const bool srcB = sg.info & I_SRC_B;
         U *dst = (U *)(srcB ? P.a_keys : P.b_keys);
         uint32_t *dstv = srcB ? P.a_vals : P.b_vals;
@@ -1005,7 +1077,7 @@ struct Sorter {
                 s->begin = b;
                 s->end = e;
                 s->pivot = 0;
-                s->pivot_v = 0;
+                s->pivot_v = (uint32_t)rwidth(P, m, bit);  // digit width of the pass
                 s->lb = pk;
                 s->lb_v = pv;
                 s->ntiles = ntiles;
@@ -1055,7 +1127,7 @@ struct Sorter {
         unsigned long long *cs = P.rslots + (size_t)sg.rslot * RDIG;
         const int64_t b = sg.begin, e = sg.end, m = e - b;
         const bool srcB = sg.info & I_SRC_B;
-        const int rbit = (int)sg.rbit, nd = rdigits(rbit);
+        const int rbit = (int)sg.rbit, nd = rdigits(sg);
         const unsigned long long c = __ldcg(&cs[tid]);
         const unsigned long long ex = block_excl_u64(c);
         if (c == (unsigned long long)m) sh.aL = tid;  // the one digit every element has
@@ -1074,6 +1146,7 @@ struct Sorter {
             if (tid == 0) {
                 Seg *gs = &P.segs[sid];
                 gs->rbit = (unsigned)(rbit + nd);
+                gs->pivot_v = (uint32_t)rwidth(P, m, rbit + nd);
                 gs->lb = pk;
                 gs->lb_v = pv;
                 gs->tiles_done = 0;
@@ -1111,7 +1184,7 @@ struct Sorter {
             sh.rl_seq = 0;
         }
         csync();
-        const int rbit = (int)sg.rbit, nd = rdigits(rbit), nrbit = rbit + nd;
+        const int rbit = (int)sg.rbit, nd = rdigits(sg), nrbit = rbit + nd;
         const bool dstB = !(sg.info & I_SRC_B);
         const int64_t cb = tid ? (int64_t)E[tid - 1] : sg.begin, ce = (int64_t)E[tid], mc = ce - cb;
         uint64_t pk = sg.lb;
@@ -1153,7 +1226,7 @@ struct Sorter {
                 s->begin = cb;
                 s->end = ce;
                 s->pivot = 0;
-                s->pivot_v = 0;
+                s->pivot_v = (uint32_t)rwidth(P, mc, nrbit);
                 s->lb = pk;
                 s->lb_v = pv;
                 s->ntiles = ntiles;
@@ -1561,7 +1634,7 @@ struct Sorter {
                     break;
                 }
                 __nanosleep(ns);
-                if (ns < 1024) ns <<= 1;
+                if (ns < PDQ_SLEEP_CAP) ns <<= 1;
             }
         }
         if (sh.nstate == 3) {
@@ -1631,6 +1704,7 @@ __global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Param
     using O = Ord<U, FLOAT>;
     __shared__ unsigned s_stop;
     const int tid = threadIdx.x;
+    pdl_trigger();  // k_init (one CTA) may be scheduled now; it waits for this grid before reading
     const U *a = (const U *)P.a_keys;
     const int64_t n = P.n;
     const int64_t CH = (int64_t)THREADS * ITEMS;
@@ -1667,6 +1741,8 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
     Shared &sh = g_sh;
     __shared__ int s_action;
     const int tid = threadIdx.x;
+    pdl_wait();     // k_check's verdict
+    pdl_trigger();  // the sorter's CTAs may be scheduled; they wait for this grid before reading
     if (tid == 0) {
         S::zero_counters();
         const unsigned bits = P.st->check_bits;
@@ -2103,8 +2179,7 @@ struct BigLeaf {
         if (tid == 0) {
             mbar_init(bar, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            sh.lq[0] = claim();
-            sh.lq[1] = sh.lq[0] == NONE ? NONE : claim();
+            sh.lq[0] = claim();  // one leaf per CTA first: a small sort spreads over every SM
             if (sh.lq[0] != NONE) prefetch(P, sh.lq[0], kd, bar);
         }
         bsync();
@@ -2116,7 +2191,7 @@ struct BigLeaf {
             if (cur == NONE) break;
             if (tid == 0) {
                 sh.lc0 = clock64();
-                sh.lq[2] = sh.lq[1] != NONE ? claim() : NONE;  // its round trip overlaps this leaf
+                sh.lq[1] = claim();  // the next leaf: prefetched once this one has left kd
             }
             pm = clock64();
             mbar_wait(bar, kphase);
@@ -2175,7 +2250,6 @@ struct BigLeaf {
                 bsync();  // every thread has read lq[0] and lq[1]
                 if (tid == 0) {
                     sh.lq[0] = sh.lq[1];
-                    sh.lq[1] = sh.lq[2];
                     sh.s_base++;
                     sh.s_bytes += (srcB ? 2ull : 1ull) * 4 * m;
                     sh.s_cyc_base += clock64() - sh.lc0;
@@ -2253,7 +2327,6 @@ struct BigLeaf {
                     sh.s_bytes += 8ull * m;
                     sh.s_cyc_base += clock64() - sh.lc0;
                     sh.lq[0] = sh.lq[1];
-                    sh.lq[1] = sh.lq[2];
                 }
                 PHASE_MARK(3);
                 bsync();
@@ -2290,7 +2363,6 @@ struct BigLeaf {
                     sh.s_bytes += 8ull * m;
                     sh.s_cyc_base += clock64() - sh.lc0;
                     sh.lq[0] = sh.lq[1];
-                    sh.lq[1] = sh.lq[2];
                 }
             }
             PHASE_MARK(3);
@@ -2687,10 +2759,15 @@ __global__ void __launch_bounds__(1024, 1) k_base_wide(const __grid_constant__ P
     using S = Sorter<U, FLOAT, KV>;
     Shared &sh = g_sh;
     const int tid = threadIdx.x;
+    pdl_wait();  // the sorter's leaf queue
     if (ld_volatile_u32(&P.st->reverse)) return;
-    if (tid == 0) S::zero_counters();
+    if (tid == 0) {
+        S::zero_counters();
+        atomicMax(&P.st->t_base_b_inv, ~globaltimer_ns());
+    }
     WideLeaf<U, FLOAT, KV>::run(P);
     if (tid == 0) {
+        atomicMax(&P.st->t_base_e, globaltimer_ns());
         atomicAdd(&P.st->c_bytes_base, sh.s_bytes);
         sh.s_bytes = 0;
         S::flush_counters(P);
@@ -2702,10 +2779,15 @@ __global__ void __launch_bounds__(BigLeaf<FLOAT>::BT, 1) k_base_big(const __grid
     using S = Sorter<uint32_t, FLOAT, false>;
     Shared &sh = g_sh;
     const int tid = threadIdx.x;
+    pdl_wait();  // the sorter's leaf queue
     if (ld_volatile_u32(&P.st->reverse)) return;
-    if (tid == 0) S::zero_counters();
+    if (tid == 0) {
+        S::zero_counters();
+        atomicMax(&P.st->t_base_b_inv, ~globaltimer_ns());
+    }
     BigLeaf<FLOAT>::run(P);
     if (tid == 0) {
+        atomicMax(&P.st->t_base_e, globaltimer_ns());
         atomicAdd(&P.st->c_bytes_base, sh.s_bytes);
         sh.s_bytes = 0;
         S::flush_counters(P);
@@ -2728,6 +2810,8 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
     using S = Sorter<U, FLOAT, KV>;
     Shared &sh = g_sh;
     const int tid = threadIdx.x;
+    pdl_wait();  // k_init's root segment and verdict
+    if (tid == 0) atomicMax(&P.st->t_sort_b_inv, ~globaltimer_ns());
 
     // K4 reverse: a non-increasing input is reversed in place (one read + one write pass)
     if (ld_volatile_u32(&P.st->reverse)) {
@@ -2744,6 +2828,8 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
                 P.a_vals[j] = y;
             }
         }
+        __syncthreads();
+        if (tid == 0) atomicMax(&P.st->t_sort_e, globaltimer_ns());
         return;
     }
     if (tid == 0) {
@@ -2816,7 +2902,10 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
         }
         csync();
     }
-    if (tid == 0) S::flush_counters(P);
+    if (tid == 0) {
+        S::flush_counters(P);
+        atomicMax(&P.st->t_sort_e, globaltimer_ns());
+    }
 }
 
 }  // namespace pdq

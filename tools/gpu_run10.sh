@@ -1,0 +1,3 @@
+PDQ_LIB=tools/libvar_wn3.so timeout 300 python tools/leaf_check.py 2>&1 | tail -1
+PDQ_LIB=tools/libvar_wn3.so timeout 300 python tools/small_n.py 2>&1
+PDQ_LIB=tools/libvar_wn3.so timeout 120 python tools/prof_sort.py 28 i32 4 2>&1 | tail -1
