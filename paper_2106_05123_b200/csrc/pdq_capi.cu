@@ -58,6 +58,12 @@ extern "C" int pdq_config_validate(const pdq_config *c) {
 namespace {
 
 constexpr int MIN_BASE = 1024;
+#ifndef PDQ_CHUNK_MAX
+#define PDQ_CHUNK_MAX 32  // tiles per ring task at most
+#endif
+#ifndef PDQ_CHUNK_DIV
+#define PDQ_CHUNK_DIV 2  // the root level gets about this many tasks per CTA
+#endif
 
 struct Layout {
     size_t b_keys, b_vals, state, segs, ring, leaves, rslots, total;
@@ -205,9 +211,9 @@ int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEven
     const int sm = smem_bytes<U, FLOAT, KV>();
     {  // tiles per task: the largest power of two <= 32 giving the root ~2 tasks per CTA
         constexpr int TL = Sorter<U, FLOAT, KV>::TL;
-        const int64_t per = ((P.n + TL - 1) / TL) / (2 * (int64_t)li.sms * li.occ);
+        const int64_t per = ((P.n + TL - 1) / TL) / (PDQ_CHUNK_DIV * (int64_t)li.sms * li.occ);
         uint32_t c = 1;
-        while (c < 32 && (int64_t)(c * 2) <= per) c *= 2;
+        while (c < PDQ_CHUNK_MAX && (int64_t)(c * 2) <= per) c *= 2;
         P.chunk = c;
     }
     if (P.use_check && P.n > 1) {

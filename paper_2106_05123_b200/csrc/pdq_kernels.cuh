@@ -164,6 +164,16 @@ struct Sorter {
     static constexpr int TL = B::TLB, IT = TL / THREADS;
     using SU = typename std::conditional<sizeof(U) == 4, int32_t, int64_t>::type;
     
+    // Tiles are relative to the segment: tile i covers [base + i TL, base + (i + 1) TL) from the segment's
+    // 16-byte-aligned base, so a segment of m elements has ceil(m / TL) tiles plus at most one (from the
+    // <= AL - 1 elements of lead-in) -- globally aligned tiles gave deep-level segments two partial tiles.
+    __device__ __forceinline__ static int64_t tile_base(int64_t b, uint32_t tile) {
+        return (b & ~(int64_t)(AL - 1)) + (int64_t)tile * TL;
+    }
+    __device__ __forceinline__ static uint32_t tiles_of(int64_t b, int64_t e) {
+        return (uint32_t)((e - (b & ~(int64_t)(AL - 1)) + TL - 1) / TL);
+    }
+
     static constexpr int KBITS = 8 * (int)sizeof(U);
     static constexpr int NBITS = KBITS + (KV ? 32 : 0);  // bits of the (ordered key, payload) composite
     __device__ __forceinline__ static bool tile_task(uint32_t type) {
@@ -376,7 +386,7 @@ struct Sorter {
             csync();
             return false;
         }
-        const uint32_t ntiles = (uint32_t)((e - 1) / TL - b / TL + 1);
+        const uint32_t ntiles = tiles_of(b, e);
         if (tid == 0) {
             uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
             sh.new_sid = sid;
@@ -423,7 +433,7 @@ struct Sorter {
             tk |= (uint64_t)((U)1 << (KBITS - 1 - bit));
         else
             tv |= 1u << (31 - (bit - KBITS));
-        const uint32_t ntiles = (uint32_t)((e - 1) / TL - b / TL + 1);
+        const uint32_t ntiles = tiles_of(b, e);
         if (tid == 0) {
             const uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
             sh.new_sid = sid;
@@ -530,7 +540,7 @@ struct Sorter {
         const long long c0 = clock64();
         if (tid < 32) warp_sample(P, b, m, srcB, perturb, depth, 0);
         csync();
-        const uint32_t ntiles = (uint32_t)((e - 1) / TL - b / TL + 1);
+        const uint32_t ntiles = tiles_of(b, e);
         if (tid == 0) {
             const uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
             sh.new_sid = sid;
@@ -607,7 +617,7 @@ struct Sorter {
         s->pivot_v = pv;
         s->lb = bd.lb;
         s->lb_v = bd.lbv;
-        s->ntiles = (uint32_t)((e - 1) / TL - b / TL + 1);
+        s->ntiles = tiles_of(b, e);
         s->info = (srcB ? I_SRC_B : 0) | (left ? I_LEFT : 0) | (bd.has_lb ? I_HAS_LB : 0) |
                   (bd.has_ub ? I_HAS_UB : 0) | (perturb ? I_PERTURB : 0) | (dup_heavy ? I_COUNT_EQ : 0);
         s->budget = budget > 0 ? budget : 0;
@@ -634,7 +644,7 @@ struct Sorter {
         const long long c0 = clock64();
         if (warp < 2) warp_sample(P, warp ? mid : b, warp ? e - mid : mid - b, srcB, perturb, depth, warp);
         csync();
-        const uint32_t ntL = (uint32_t)((mid - 1) / TL - b / TL + 1), ntR = (uint32_t)((e - 1) / TL - mid / TL + 1);
+        const uint32_t ntL = tiles_of(b, mid), ntR = tiles_of(mid, e);
         const uint32_t nkL = seg_ntasks(ntL, P.chunk), nkR = seg_ntasks(ntR, P.chunk);
         if (tid == 0) {
             const uint32_t sidL = (uint32_t)reuse_sid, sidR = atomicAdd(&P.st->seg_alloc, 1u);
@@ -834,7 +844,7 @@ struct Sorter {
         const int tid = threadIdx.x;
         const Seg &sg = sh.seg;
         const int64_t b = sg.begin, e = sg.end;
-        const int64_t tbase = (b / TL + tile) * (int64_t)TL;
+        const int64_t tbase = tile_base(b, tile);
         const int lo_i = (int)((b > tbase ? b : tbase) - tbase), hi_i = (int)((e < tbase + TL ? e : tbase + TL) - tbase);
         const int st = (int)(ci % B::NSTAGE);
         const U *sk = B::stage(st);
@@ -893,7 +903,7 @@ struct Sorter {
         const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
         const Seg &sg = sh.seg;
         const int64_t b = sg.begin, e = sg.end;
-        const int64_t tbase = (b / TL + tile) * (int64_t)TL;
+        const int64_t tbase = tile_base(b, tile);
         const int lo_i = (int)((b > tbase ? b : tbase) - tbase), hi_i = (int)((e < tbase + TL ? e : tbase + TL) - tbase);
         const int st = (int)(ci % B::NSTAGE);
         U *sk = B::stage(st);
@@ -1066,7 +1076,7 @@ struct Sorter {
         P.rslots[(size_t)slot * RDIG + tid] = 0ull;  // THREADS == RDIG
         __threadfence();
         csync();
-        const uint32_t ntiles = (uint32_t)((e - 1) / TL - b / TL + 1);
+        const uint32_t ntiles = tiles_of(b, e);
         if (tid == 0) {
             const uint32_t sid = reuse_sid >= 0 ? (uint32_t)reuse_sid : atomicAdd(&P.st->seg_alloc, 1u);
             sh.new_sid = sid;
@@ -1221,7 +1231,7 @@ struct Sorter {
             } else {
                 unsigned long long *ccs = P.rslots + (size_t)slot * RDIG;
                 for (int q = 0; q < RDIG; ++q) ccs[q] = 0ull;
-                const uint32_t ntiles = (uint32_t)((ce - 1) / TL - cb / TL + 1);
+                const uint32_t ntiles = tiles_of(cb, ce);
                 Seg *s = &P.segs[csid];
                 s->begin = cb;
                 s->end = ce;
@@ -1283,7 +1293,7 @@ struct Sorter {
         const bool srcB = sg.info & I_SRC_B;
         const U *src = (const U *)(srcB ? P.b_keys : P.a_keys);
         const uint32_t *srcv = srcB ? P.b_vals : P.a_vals;
-        const int64_t tbase = (b / TL + tile) * (int64_t)TL;
+        const int64_t tbase = tile_base(b, tile);
         const int64_t lo = b > tbase ? b : tbase;
         const int64_t hi = e < tbase + TL ? e : tbase + TL;
         const int64_t nfl = P.n & ~(int64_t)(AL - 1);
@@ -1470,7 +1480,7 @@ struct Sorter {
         const bool left_mode = sg.info & I_LEFT;
         const bool count_eq = (sg.info & I_COUNT_EQ) && !left_mode;
         const bool packed = (e - b) < (1ll << 32);
-        const int64_t tbase = (b / TL + tile) * (int64_t)TL;
+        const int64_t tbase = tile_base(b, tile);
         const int64_t lo = b > tbase ? b : tbase;
         const int64_t hi = e < tbase + TL ? e : tbase + TL;
         const int st = (int)(ci % B::NSTAGE);
@@ -1654,7 +1664,7 @@ struct Sorter {
 
     __device__ static void fill_tile(const Params &P, const Seg &sg, uint32_t tile) {
         Shared &sh = g_sh;
-        const int64_t tbase = (sg.begin / TL + tile) * (int64_t)TL;
+        const int64_t tbase = tile_base(sg.begin, tile);
         const int64_t lo = sg.begin > tbase ? sg.begin : tbase;
         const int64_t hi = sg.end < tbase + TL ? sg.end : tbase + TL;
         const U raw = O::from((U)sg.pivot);
