@@ -8,6 +8,8 @@
 
 #include <mutex>
 
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a profiler is attached
+
 #include "../../include/pdq_b200.h"
 #include "pdq_bucket.cuh"
 #include "pdq_kernels.cuh"
@@ -139,16 +141,21 @@ int smem_bytes() {
     return Bufs<U, KV>::bytes();
 }
 
+constexpr int MAX_DEVS = 64;
+
 template <class U, bool FLOAT, bool KV>
 cudaError_t prepare(LaunchInfo &li) {
+    // per device and element type: kernel attributes set once, occupancy and SM count cached
     static std::mutex mu;
-    static int cached_dev = -1;
-    static LaunchInfo cached;
+    static bool ready[MAX_DEVS] = {};
+    static LaunchInfo cache[MAX_DEVS];
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= MAX_DEVS) return cudaErrorInvalidDevice;
     std::lock_guard<std::mutex> g(mu);
-    if (cached_dev != dev) {
+    LaunchInfo &cached = cache[dev];
+    if (!ready[dev]) {
         const int sm = smem_bytes<U, FLOAT, KV>();
         if ((e = cudaFuncSetAttribute(k_sort<U, FLOAT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) !=
             cudaSuccess)
@@ -175,7 +182,7 @@ cudaError_t prepare(LaunchInfo &li) {
             cudaSuccess)
             return e;
         if (cached.occ < 1) cached.occ = 1;
-        cached_dev = dev;
+        ready[dev] = true;
     }
     li = cached;
     return cudaSuccess;
@@ -282,6 +289,10 @@ extern "C" int pdq_sort_timed(void *keys, int dtype, uint32_t *payload, int64_t 
     if (((uintptr_t)workspace & 255)) return set_err(PDQ_ERR_ALIGN, "workspace must be 256-byte aligned%s");
     cudaStream_t s = (cudaStream_t)stream;
     unsigned char *ws = (unsigned char *)workspace;
+    struct Range {  // NVTX range over the enqueue (SURVEY §5 tracing)
+        Range() { nvtxRangePushA("pdq_sort"); }
+        ~Range() { nvtxRangePop(); }
+    } range;
     if (evs) cudaEventRecord(evs, s);
     cudaError_t e = cudaMemsetAsync(ws + L.state, 0, sizeof(State), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(ws + L.ring, 0xFF, (size_t)(1ull << L.log_q) * 8, s);
@@ -377,6 +388,8 @@ extern "C" size_t pdq_bucket_workspace_bytes(int64_t n, int nbuckets) {
     return a256((size_t)nbuckets * (size_t)BK_MAX_CTAS * sizeof(int64_t));  // any element type's grid
 }
 
+__global__ void k_set_i64(int64_t *p, int64_t v) { *p = v; }
+
 namespace {
 template <class U, bool FLOAT, bool KV, int LT>
 int launch_bucket(const void *keys, const uint32_t *vals, int64_t n, int64_t gidx_base, const void *sk,
@@ -386,10 +399,12 @@ int launch_bucket(const void *keys, const uint32_t *vals, int64_t n, int64_t gid
     const int nb = ns + 1;
     const size_t hist = (size_t)nb * BK_THREADS * sizeof(uint32_t);
     const size_t sc = sizeof(ScatterSmem<U, KV>) + hist;
-    cudaFuncSetAttribute(k_bucket_count<U, FLOAT, KV, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(BK_MAX * BK_THREADS * sizeof(uint32_t)));
-    cudaFuncSetAttribute(k_bucket_scatter<U, FLOAT, KV, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(ScatterSmem<U, KV>) + BK_MAX * BK_THREADS * sizeof(uint32_t)));
+    cudaError_t ea = cudaFuncSetAttribute(k_bucket_count<U, FLOAT, KV, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(BK_MAX * BK_THREADS * sizeof(uint32_t)));
+    if (ea == cudaSuccess)
+        ea = cudaFuncSetAttribute(k_bucket_scatter<U, FLOAT, KV, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(ScatterSmem<U, KV>) + BK_MAX * BK_THREADS * sizeof(uint32_t)));
+    if (ea != cudaSuccess) return set_err(PDQ_ERR_CUDA, "bucket setup: %s", cudaGetErrorString(ea));
     k_bucket_count<U, FLOAT, KV, LT><<<g.ctas, BK_THREADS, hist, s>>>((const U *)keys, vals, n, gidx_base,
                                                                          (const U *)sk, sv, sg, ns, cnt, g);
     k_bucket_scan<<<1, BK_SCAN_THREADS, 0, s>>>(cnt, (int64_t)nb * g.ctas, nb, g.ctas, bucket_counts);
@@ -445,8 +460,10 @@ extern "C" int pdq_bucket(const void *keys, int dtype, const uint32_t *payload, 
         cudaError_t e = cudaMemcpyAsync(out_keys, keys, (size_t)n * dtype_size(dtype), cudaMemcpyDeviceToDevice, s);
         if (e == cudaSuccess && payload)
             e = cudaMemcpyAsync(out_payload, payload, (size_t)n * 4, cudaMemcpyDeviceToDevice, s);
-        if (e == cudaSuccess)  // pageable source: staged before the call returns
-            e = cudaMemcpyAsync(bucket_counts, &cn, sizeof(cn), cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) {  // the one bucket's size, written by the device (no host staging)
+            k_set_i64<<<1, 1, 0, s>>>(bucket_counts, cn);
+            e = cudaGetLastError();
+        }
         return e == cudaSuccess ? PDQ_OK : set_err(PDQ_ERR_CUDA, "bucket copy: %s", cudaGetErrorString(e));
     }
     int64_t *cnt = (int64_t *)workspace;

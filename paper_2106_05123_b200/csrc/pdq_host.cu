@@ -26,6 +26,8 @@
 
 #include "../../include/pdq_b200.h"
 
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a profiler is attached
+
 #if defined(__x86_64__)
 #include <emmintrin.h>
 #endif
@@ -323,7 +325,9 @@ extern "C" int pdq_host_sort(pdq_host_sorter *h, void *keys, int dtype, uint32_t
     if ((e = cudaEventRecord(h->ev_t0, h->stream)) != cudaSuccess) return fail(h, "event", e);
     for (Worker &wk : h->w)  // worker streams start after anything earlier on the sort stream
         if ((e = cudaStreamWaitEvent(wk.stream, h->ev_t0, 0)) != cudaSuccess) return fail(h, "stream wait", e);
+    nvtxRangePushA("pdq_host_sort h2d");
     run_all(h, [&](int id) { h2d_worker(h, id, ch); });
+    nvtxRangePop();
     for (Worker &wk : h->w) {
         if (wk.rc) return wk.rc;
         if ((e = cudaStreamWaitEvent(h->stream, wk.done, 0)) != cudaSuccess) return fail(h, "join h2d", e);
@@ -341,7 +345,9 @@ extern "C" int pdq_host_sort(pdq_host_sorter *h, void *keys, int dtype, uint32_t
     const auto t2 = std::chrono::steady_clock::now();
 
     // 3. D2H through the pinned slots into the caller's buffers
+    nvtxRangePushA("pdq_host_sort d2h");
     run_all(h, [&](int id) { d2h_worker(h, id, ch); });
+    nvtxRangePop();
     for (Worker &wk : h->w)
         if (wk.rc) return wk.rc;
     const auto t3 = std::chrono::steady_clock::now();

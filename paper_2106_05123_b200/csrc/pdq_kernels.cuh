@@ -1318,6 +1318,12 @@ struct Sorter {
     }
 
     // ---- K2/K3: one partition tile (compute warps) ------------------------------------------------
+    __device__ __forceinline__ static void stvec(U *g, const U (&x)[VEC]) {
+        if constexpr (sizeof(U) == 4)
+            *reinterpret_cast<uint4 *>(g) = make_uint4(x[0], x[1], x[2], x[3]);
+        else
+            *reinterpret_cast<ulonglong2 *>(g) = make_ulonglong2(x[0], x[1]);
+    }
     __device__ __forceinline__ static void ldvec(const U *s, int q, U (&x)[VEC]) {
         if constexpr (sizeof(U) == 4) {
             const uint4 y = reinterpret_cast<const uint4 *>(s)[q];
@@ -2826,9 +2832,42 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
     // K4 reverse: a non-increasing input is reversed in place (one read + one write pass)
     if (ld_volatile_u32(&P.st->reverse)) {
         U *a = (U *)P.a_keys;
-        const int64_t half = P.n / 2;
-        for (int64_t i = (int64_t)blockIdx.x * THREADS + tid; i < half; i += (int64_t)gridDim.x * THREADS) {
-            const int64_t j = P.n - 1 - i;
+        const int64_t n = P.n, half = n / 2;
+        const int64_t gt = (int64_t)blockIdx.x * THREADS + tid, gs = (int64_t)gridDim.x * THREADS;
+        int64_t done = 0;
+        if (n % S::AL == 0) {
+            // 16-byte vectors from both ends (the array and its end are then 16-byte aligned): vector c of
+            // the front swaps with vector c of the back, each reversed in registers
+            constexpr int V = S::VEC;
+            const int64_t nv = half / S::AL * S::AL / V;  // key vectors per side (whole payload vectors too)
+            for (int64_t c = gt; c < nv; c += gs) {
+                U *f = a + c * V, *bk = a + n - (c + 1) * V;
+                U x[V], y[V];
+                S::ldvec(f, 0, x);
+                S::ldvec(bk, 0, y);
+                U rx[V], ry[V];
+#pragma unroll
+                for (int q = 0; q < V; ++q) {
+                    rx[q] = x[V - 1 - q];
+                    ry[q] = y[V - 1 - q];
+                }
+                S::stvec(f, ry);
+                S::stvec(bk, rx);
+            }
+            if (KV) {
+                const int64_t nw = half / S::AL * S::AL / 4;
+                for (int64_t c = gt; c < nw; c += gs) {
+                    uint4 *f = reinterpret_cast<uint4 *>(P.a_vals + c * 4);
+                    uint4 *bk = reinterpret_cast<uint4 *>(P.a_vals + n - (c + 1) * 4);
+                    const uint4 x = *f, y = *bk;
+                    *f = make_uint4(y.w, y.z, y.y, y.x);
+                    *bk = make_uint4(x.w, x.z, x.y, x.x);
+                }
+            }
+            done = half / S::AL * S::AL;
+        }
+        for (int64_t i = done + gt; i < half; i += gs) {  // the rest (or all of an unaligned length)
+            const int64_t j = n - 1 - i;
             U x = a[i];
             a[i] = a[j];
             a[j] = x;
