@@ -295,7 +295,9 @@ extern "C" int pdq_sort_timed(void *keys, int dtype, uint32_t *payload, int64_t 
     } range;
     if (evs) cudaEventRecord(evs, s);
     cudaError_t e = cudaMemsetAsync(ws + L.state, 0, sizeof(State), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ws + L.ring, 0xFF, (size_t)(1ull << L.log_q) * 8, s);
+    // the ring is emptied by k_check when it runs (one fewer stream operation on the latency path)
+    const bool check_kernel = cfg.use_partial_insertion && n > 1;
+    if (e == cudaSuccess && !check_kernel) e = cudaMemsetAsync(ws + L.ring, 0xFF, (size_t)(1ull << L.log_q) * 8, s);
     if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
     if (n == 0) {  // finish() reads a zeroed state: status 0
         if (ev0) cudaEventRecord(ev0, s);

@@ -1721,6 +1721,12 @@ __global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Param
     __shared__ unsigned s_stop;
     const int tid = threadIdx.x;
     pdl_trigger();  // k_init (one CTA) may be scheduled now; it waits for this grid before reading
+    {  // the task ring starts empty (all-ones words match no round tag); k_init pushes after this grid
+        uint4 *r4 = reinterpret_cast<uint4 *>(P.ring);
+        const int64_t words = (1ll << P.log_q) / 2;
+        for (int64_t i = (int64_t)blockIdx.x * THREADS + tid; i < words; i += (int64_t)gridDim.x * THREADS)
+            r4[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    }
     const U *a = (const U *)P.a_keys;
     const int64_t n = P.n;
     const int64_t CH = (int64_t)THREADS * ITEMS;
