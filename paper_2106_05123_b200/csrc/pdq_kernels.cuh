@@ -2406,7 +2406,7 @@ struct WideLeaf {
     using O = Ord<U, FLOAT>;
     using H = BigLeaf<false>;  // the 1024-thread block helpers
     static constexpr int BT = 1024, BI = 8, CAP = BT * BI;
-    static constexpr int BBK = 4096, LOG_BK = 12;
+    static constexpr int BBK = 8192, LOG_BK = 13;  // ~1 element per bucket: short, rarely divergent rank loops
     static constexpr int CMAX = 32;  // largest bucket ranked by comparisons; beyond it the leaf takes radix passes
     static constexpr int KB = (CAP + 16) * (int)sizeof(U), VB = KV ? (CAP + 16) * 4 : 0;
     static constexpr int KCK = 0, KCV = KB, KDK = KB + VB, KDV = 2 * KB + VB, CNT = 2 * KB + 2 * VB,
@@ -2423,50 +2423,6 @@ struct WideLeaf {
     __device__ __forceinline__ static int eidx(int j, int off) {
         return 4 * ((j >> 2) * BT + (int)threadIdx.x) + (j & 3) - off;
     }
-    __device__ __forceinline__ static void load(const Params &P, uint64_t lf, U (&xs)[BI], uint32_t (&vs)[BI]) {
-        const int tid = threadIdx.x;
-        const int m = lf == ~0ull ? 0 : (int)((lf >> 1) & 0x7FFF) + 1;
-        const int64_t b = (int64_t)(lf >> 16);
-        const int off = (int)(b & 3);
-        const U *src = (const U *)((lf & 1u) ? P.b_keys : P.a_keys) + (b - off);
-        const uint32_t *srcv = KV ? ((lf & 1u) ? P.b_vals : P.a_vals) + (b - off) : nullptr;
-        const int64_t room = P.n - (b - off);
-#pragma unroll
-        for (int jv = 0; jv < BI / 4; ++jv) {
-            const int e0 = 4 * (jv * BT + tid);
-            U k4[4] = {0, 0, 0, 0};
-            uint32_t v4[4] = {0, 0, 0, 0};
-            if (m > 0 && e0 < off + m && e0 + 4 > off) {
-                if (e0 + 4 <= room) {
-                    if constexpr (sizeof(U) == 4) {
-                        const uint4 y = __ldcg(reinterpret_cast<const uint4 *>(src + e0));
-                        k4[0] = (U)y.x; k4[1] = (U)y.y; k4[2] = (U)y.z; k4[3] = (U)y.w;
-                    } else {
-                        const ulonglong2 y0 = __ldcg(reinterpret_cast<const ulonglong2 *>(src + e0));
-                        const ulonglong2 y1 = __ldcg(reinterpret_cast<const ulonglong2 *>(src + e0 + 2));
-                        k4[0] = (U)y0.x; k4[1] = (U)y0.y; k4[2] = (U)y1.x; k4[3] = (U)y1.y;
-                    }
-                    if constexpr (KV) {
-                        const uint4 z = __ldcg(reinterpret_cast<const uint4 *>(srcv + e0));
-                        v4[0] = z.x; v4[1] = z.y; v4[2] = z.z; v4[3] = z.w;
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (e0 + q < room) {
-                            k4[q] = ldcg(src + e0 + q);
-                            if constexpr (KV) v4[q] = ldcg(srcv + e0 + q);
-                        }
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                xs[4 * jv + q] = k4[q];
-                vs[4 * jv + q] = v4[q];
-            }
-        }
-    }
-
     __device__ __forceinline__ static bool less(U a, uint32_t va, U b, uint32_t vb) {
         return a < b || (KV && a == b && va < vb);
     }
@@ -2569,48 +2525,135 @@ struct WideLeaf {
         }
     }
 
+    // thread 0: TMA bulk loads of leaf `lf` (keys, and payloads) into kd / vd from its 16-byte aligned base
+    // (4-element granularity keeps both arrays' copies multiples of 16 bytes; the array's last partial
+    // vector by scalar loads), completing on `bar`
+    __device__ __forceinline__ static void prefetch(const Params &P, uint64_t lf, uint64_t *bar) {
+        const int m = (int)((lf >> 1) & 0x7FFF) + 1;
+        const int64_t b = (int64_t)(lf >> 16);
+        const int off = (int)(b & 3);
+        const int64_t base = b - off;
+        const U *src = (const U *)((lf & 1u) ? P.b_keys : P.a_keys) + base;
+        const uint32_t *srcv = KV ? ((lf & 1u) ? P.b_vals : P.a_vals) + base : nullptr;
+        U *kd = kdk();
+        uint32_t *vd = kdv();
+        const int64_t vec = ((int64_t)(off + m) + 3) & ~(int64_t)3;
+        const int64_t room = P.n - base;
+        const int64_t bulk = vec < (room & ~(int64_t)3) ? vec : (room & ~(int64_t)3);
+        for (int64_t e = bulk; e < vec && e < room; ++e) {
+            kd[e] = ldcg(src + e);
+            if constexpr (KV) vd[e] = ldcg(srcv + e);
+        }
+        fence_proxy_async();
+        mbar_expect_tx(bar, (unsigned)(bulk * (int64_t)(sizeof(U) + (KV ? 4 : 0))));
+        if (bulk > 0) {
+            bulk_g2s(kd, src, (unsigned)(bulk * sizeof(U)), bar);
+            if constexpr (KV) bulk_g2s(vd, srcv, (unsigned)(bulk * 4), bar);
+        }
+    }
+    // every thread: its registers of leaf `lf` from kd / vd (the 16-byte vector layout of eidx)
+    __device__ __forceinline__ static void read_kd(uint64_t lf, U (&xs)[BI], uint32_t (&vs)[BI]) {
+        const int tid = threadIdx.x;
+        const int m = (int)((lf >> 1) & 0x7FFF) + 1;
+        const int off = (int)((lf >> 16) & 3);
+        const U *kd = kdk();
+        const uint32_t *vd = kdv();
+#pragma unroll
+        for (int jv = 0; jv < BI / 4; ++jv) {
+            const int e0 = 4 * (jv * BT + tid);
+            U k4[4] = {0, 0, 0, 0};
+            uint32_t v4[4] = {0, 0, 0, 0};
+            if (e0 < off + m) {
+                if constexpr (sizeof(U) == 4) {
+                    const uint4 y = *reinterpret_cast<const uint4 *>(kd + e0);
+                    k4[0] = (U)y.x; k4[1] = (U)y.y; k4[2] = (U)y.z; k4[3] = (U)y.w;
+                } else {
+                    const ulonglong2 y0 = *reinterpret_cast<const ulonglong2 *>(kd + e0);
+                    const ulonglong2 y1 = *reinterpret_cast<const ulonglong2 *>(kd + e0 + 2);
+                    k4[0] = (U)y0.x; k4[1] = (U)y0.y; k4[2] = (U)y1.x; k4[3] = (U)y1.y;
+                }
+                if constexpr (KV) {
+                    const uint4 z = *reinterpret_cast<const uint4 *>(vd + e0);
+                    v4[0] = z.x; v4[1] = z.y; v4[2] = z.z; v4[3] = z.w;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                xs[4 * jv + q] = k4[q];
+                vs[4 * jv + q] = v4[q];
+            }
+        }
+    }
+
+    // Leaves of <= CAP - 4 elements, one per CTA at a time: the next leaf is prefetched into kd / vd by
+    // TMA while the current one is bucketed into kc / vc (at q = a0 + position, a0 = b mod 4, the 16-byte
+    // phase of the leaf in A), ranked in place inside its bucket (keys + payloads held in registers
+    // across one barrier) and copied out to A by consecutive threads in 16-byte chunks.  A leaf with a
+    // bucket of more than CMAX elements (e.g. argsort of low-cardinality keys) takes stable LSD radix
+    // passes (they use kd, so the prefetch is waited for and issued again afterwards).
     __device__ static void run(const Params &P) {
         Shared &sh = g_sh;
         const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-        U *kc = kck(), *kd = kdk();
-        uint32_t *vc = kcv(), *vd = kdv(), *cn = cnt();
+        U *kc = kck();
+        uint32_t *vc = kcv(), *cn = cnt();
         uint64_t *rd = red();
-        unsigned long long count = *(volatile unsigned long long *)&P.st->leaf_count;
-        if (count > P.leaf_cap) count = P.leaf_cap;
         constexpr uint64_t NONE = ~0ull;
-        if (tid == 0) {
+        uint64_t *bar = &sh.bar[0];
+        auto claim = [&]() -> uint64_t {  // thread 0
+            unsigned long long count = *(volatile unsigned long long *)&P.st->leaf_count;
+            if (count > P.leaf_cap) count = P.leaf_cap;
             const unsigned long long idx = atomicAdd(&P.st->leaf_next, 1ull);
-            sh.lf[0] = idx < count ? ldcg(P.leaves + idx) : NONE;
+            return idx < count ? ldcg(P.leaves + idx) : NONE;
+        };
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            sh.lq[0] = claim();
+            if (sh.lq[0] != NONE) prefetch(P, sh.lq[0], bar);
         }
         H::bsync();
-        uint64_t cur = sh.lf[0];
-        int k = 0;
+        unsigned kphase = 0;
         U xs[BI];
         uint32_t vs[BI];
-        load(P, cur, xs, vs);
-        while (cur != NONE) {
-            const long long c0 = clock64();
-            uint64_t pend = NONE;
+        for (;;) {
+            const uint64_t cur = sh.lq[0];
+            if (cur == NONE) break;
             if (tid == 0) {
-                const unsigned long long idx = atomicAdd(&P.st->leaf_next, 1ull);
-                if (idx < count) pend = ldcg(P.leaves + idx);
+                sh.lc0 = clock64();
+                sh.lq[1] = claim();
             }
+            mbar_wait(bar, kphase);
+            kphase ^= 1u;
+            read_kd(cur, xs, vs);
             const int m = (int)((cur >> 1) & 0x7FFF) + 1;
             const int64_t b = (int64_t)(cur >> 16);
             const bool srcB = cur & 1u;
             const int off = (int)(b & 3);
-            reinterpret_cast<uint4 *>(cn)[tid] = make_uint4(0, 0, 0, 0);  // BBK = 4 BT counters
+            {
+                uint4 *c4 = reinterpret_cast<uint4 *>(cn);
+#pragma unroll
+                for (int q = 0; q < BBK / 4 / BT; ++q) c4[q * BT + tid] = make_uint4(0, 0, 0, 0);
+            }
+            const int nvec = (off + m + 4 * BT - 1) / (4 * BT);  // vectors holding leaf elements (CTA-uniform)
             U kmn = ~(U)0, kmx = 0;
             uint32_t vmn = 0xFFFFFFFFu, vmx = 0;
 #pragma unroll
-            for (int j = 0; j < BI; ++j) {
-                if ((unsigned)eidx(j, off) < (unsigned)m) {
-                    const U x = O::to(xs[j]);
-                    xs[j] = x;
-                    kmn = x < kmn ? x : kmn;
-                    kmx = x > kmx ? x : kmx;
-                    vmn = min(vmn, vs[j]);
-                    vmx = max(vmx, vs[j]);
+            for (int jv = 0; jv < BI / 4; ++jv) {
+                if (jv < nvec) {
+                    const int e0 = 4 * (jv * BT + tid) - off;
+                    const bool whole = e0 >= 0 && e0 + 4 <= m;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int j = 4 * jv + q;
+                        if (whole || (unsigned)(e0 + q) < (unsigned)m) {
+                            const U x = O::to(xs[j]);
+                            xs[j] = x;
+                            kmn = x < kmn ? x : kmn;
+                            kmx = x > kmx ? x : kmx;
+                            vmn = min(vmn, vs[j]);
+                            vmx = max(vmx, vs[j]);
+                        }
+                    }
                 }
             }
 #pragma unroll
@@ -2627,7 +2670,8 @@ struct WideLeaf {
                 rd[64 + warp] = vmn;
                 rd[96 + warp] = vmx;
             }
-            H::bsync();
+            H::bsync();  // kd / vd have been read by every thread: the next leaf may land in them
+            if (tid == 0 && sh.lq[1] != NONE) prefetch(P, sh.lq[1], bar);
             {  // lane q reads warp q's extremes; one warp reduction (every warp computes the same)
                 kmn = (U)rd[lane];
                 kmx = (U)rd[32 + lane];
@@ -2652,16 +2696,14 @@ struct WideLeaf {
                             if constexpr (KV) P.a_vals[b + eidx(j, off)] = vs[j];
                         }
                 }
+                H::bsync();  // every thread has read lq[0] and lq[1]
                 if (tid == 0) {
-                    sh.lf[k ^ 1] = pend;
+                    sh.lq[0] = sh.lq[1];
                     sh.s_base++;
                     sh.s_bytes += (srcB ? 2ull : 1ull) * (sizeof(U) + (KV ? 4 : 0)) * m;
-                    sh.s_cyc_base += clock64() - c0;
+                    sh.s_cyc_base += clock64() - sh.lc0;
                 }
                 H::bsync();
-                cur = sh.lf[k ^ 1];
-                load(P, cur, xs, vs);
-                k ^= 1;
                 continue;
             }
             // bucket source: the key, or the payload when every key is equal
@@ -2677,99 +2719,185 @@ struct WideLeaf {
             };
             uint32_t pp[BI / 2];
 #pragma unroll
-            for (int j = 0; j < BI; ++j) {
-                const uint32_t sl =
-                    ((unsigned)eidx(j, off) < (unsigned)m) ? atomicAdd(&cn[bucket(xs[j], vs[j])], 1u) : 0u;
-                if (j & 1) pp[j / 2] |= sl << 16;
-                else pp[j / 2] = sl;
+            for (int jv = 0; jv < BI / 4; ++jv) {
+                pp[2 * jv] = pp[2 * jv + 1] = 0;
+                if (jv < nvec) {
+                    const int e0 = 4 * (jv * BT + tid) - off;
+                    const bool whole = e0 >= 0 && e0 + 4 <= m;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int j = 4 * jv + q;
+                        if (whole || (unsigned)(e0 + q) < (unsigned)m)
+                            pp[j / 2] |= atomicAdd(&cn[bucket(xs[j], vs[j])], 1u) << ((j & 1) << 4);
+                    }
+                }
             }
             H::bsync();
             uint32_t cmax;
-            {  // (start, count) words: thread t owns buckets [4t, 4t + 4)
-                uint4 *c4 = reinterpret_cast<uint4 *>(cn) + tid;
-                const uint4 y = *c4;
-                const uint32_t tot = y.x + y.y + y.z + y.w;
-                const uint32_t mc = max(max(y.x, y.y), max(y.z, y.w));
+            {  // (start, count) words: thread t owns buckets [PB t, PB t + PB)
+                constexpr int PB = BBK / BT;
+                uint4 *c4 = reinterpret_cast<uint4 *>(cn + PB * tid);
+                uint32_t tot = 0, mc = 0;
+#pragma unroll
+                for (int q = 0; q < PB / 4; ++q) {
+                    const uint4 y = c4[q];
+                    tot += y.x + y.y + y.z + y.w;
+                    mc = max(mc, max(max(y.x, y.y), max(y.z, y.w)));
+                }
                 uint32_t run = H::block_excl_scan(tot, reinterpret_cast<uint32_t *>(rd) + 128, mc, &cmax);
-                uint4 w;
-                w.x = run | (y.x << 16); run += y.x;
-                w.y = run | (y.y << 16); run += y.y;
-                w.z = run | (y.z << 16); run += y.z;
-                w.w = run | (y.w << 16);
-                *c4 = w;
-            }
-            H::bsync();
 #pragma unroll
-            for (int j = 0; j < BI; ++j) {
-                if ((unsigned)eidx(j, off) < (unsigned)m) {
-                    const uint32_t pos = (cn[bucket(xs[j], vs[j])] & 0xFFFFu) + ((pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu);
-                    PDQ_CHECK(pos < (uint32_t)m, "wide leaf scatter slot");
-                    kc[pos] = xs[j];
-                    if constexpr (KV) vc[pos] = vs[j];
+                for (int q = 0; q < PB / 4; ++q) {
+                    const uint4 y = c4[q];
+                    uint4 o;
+                    o.x = run | (y.x << 16); run += y.x;
+                    o.y = run | (y.y << 16); run += y.y;
+                    o.z = run | (y.z << 16); run += y.z;
+                    o.w = run | (y.w << 16); run += y.w;
+                    c4[q] = o;
                 }
             }
-            const int a0 = off;
-            if (tid == 0) {
-                bulk_wait_read();  // the previous leaf's bulk stores have left kd / vd
-                sh.lf[k ^ 1] = pend;
-            }
+            if (tid == 0) bulk_wait_read();  // a slow leaf's bulk store has left kd (its prefetch follows it)
             H::bsync();
-            const uint64_t nxt = sh.lf[k ^ 1];
-            if (cmax > (uint32_t)CMAX) {
-                // clustered leaf (typically many equal keys with distinct payloads): stable radix passes
-                radix_leaf(m, a0, kmn, krange, vmn, vmx - vmn);
-                load(P, nxt, xs, vs);
-            } else {
-            load(P, nxt, xs, vs);  // the next leaf's loads fly while this one is ranked and stored
+            const bool fast = cmax <= (uint32_t)CMAX;
+            const int a0 = fast ? off : 0;  // fast path: q-space (the 16-byte phase of A); slow: linear
 #pragma unroll
-            for (int j = 0; j < BI; ++j) {
-                if (j * BT + tid < m) {
-                    const uint32_t p = j * BT + tid;
-                    const U x = kc[p];
-                    const uint32_t v = KV ? vc[p] : 0u;
-                    const uint32_t sc = cn[bucket(x, v)];
-                    const uint32_t s0 = sc & 0xFFFFu, e = s0 + (sc >> 16);
-                    uint32_t r = s0;
-                    for (uint32_t i = s0; i < e; ++i) {  // ranks among the bucket ((key, payload) order)
-                        const U y = kc[i];
-                        const uint32_t w = KV ? vc[i] : 0u;
-                        r += less(y, w, x, v) | ((y == x) & (w == v) & (i < p));
+            for (int jv = 0; jv < BI / 4; ++jv) {
+                if (jv < nvec) {
+                    const int e0 = 4 * (jv * BT + tid) - off;
+                    const bool whole = e0 >= 0 && e0 + 4 <= m;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int j = 4 * jv + q;
+                        if (whole || (unsigned)(e0 + q) < (unsigned)m) {
+                            const uint32_t pos = (cn[bucket(xs[j], vs[j])] & 0xFFFFu) + ((pp[j / 2] >> ((j & 1) << 4)) & 0xFFFFu);
+                            PDQ_CHECK(pos < (uint32_t)m, "wide leaf scatter slot");
+                            kc[a0 + pos] = xs[j];
+                            if constexpr (KV) vc[a0 + pos] = vs[j];
+                        }
                     }
-                    PDQ_CHECK(r < (uint32_t)m, "wide leaf rank");
-                    kd[a0 + r] = O::from(x);
-                    if constexpr (KV) vd[a0 + r] = v;
                 }
             }
+            H::bsync();
+            if (fast) {
+                // rank every element inside its bucket ((key, payload) order, ties by position), then
+                // write it to its rank in place (all reads precede the barrier)
+                uint32_t rk[BI];
+#pragma unroll
+                for (int j = 0; j < BI; ++j) {
+                    const int p = j * BT + tid;
+                    rk[j] = 0xFFFFFFFFu;
+                    if (p < m) {
+                        const U x = kc[a0 + p];
+                        const uint32_t v = KV ? vc[a0 + p] : 0u;
+                        const uint32_t sc = cn[bucket(x, v)];
+                        const uint32_t s0 = sc & 0xFFFFu, c = sc >> 16;
+                        uint32_t r = s0;
+                        if (c > 1) {
+                            for (uint32_t i = s0; i < s0 + c; ++i) {
+                                const U y = kc[a0 + i];
+                                const uint32_t w = KV ? vc[a0 + i] : 0u;
+                                r += less(y, w, x, v) | ((y == x) & (w == v) & (i < (uint32_t)p));
+                            }
+                        }
+                        PDQ_CHECK(r < (uint32_t)m, "wide leaf rank");
+                        rk[j] = r;
+                        xs[j] = x;
+                        vs[j] = v;
+                    }
+                }
+                H::bsync();
+#pragma unroll
+                for (int j = 0; j < BI; ++j) {
+                    if (rk[j] != 0xFFFFFFFFu) {
+                        kc[a0 + rk[j]] = xs[j];
+                        if constexpr (KV) vc[a0 + rk[j]] = vs[j];
+                    }
+                }
+                H::bsync();
+                // copy-out: 16-byte chunks of q-space (a0 + m slots) to A + b - a0, raw keys
+                U *dstk = (U *)P.a_keys + (b - a0);
+                const uint32_t qend = (uint32_t)(a0 + m);
+                constexpr int KPC = 16 / (int)sizeof(U);  // keys per 16-byte chunk
+                for (uint32_t c = tid; c < (qend + KPC - 1) / KPC; c += BT) {
+                    const uint32_t q = c * KPC;
+                    if (q >= (uint32_t)a0 && q + KPC <= qend) {
+                        if constexpr (sizeof(U) == 4) {
+                            const uint4 y = *reinterpret_cast<const uint4 *>(kc + q);
+                            *reinterpret_cast<uint4 *>(dstk + q) =
+                                make_uint4(O::from(y.x), O::from(y.y), O::from(y.z), O::from(y.w));
+                        } else {
+                            const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(kc + q);
+                            *reinterpret_cast<ulonglong2 *>(dstk + q) = make_ulonglong2(O::from(y.x), O::from(y.y));
+                        }
+                    } else {
+                        for (int e = 0; e < KPC; ++e)
+                            if (q + e >= (uint32_t)a0 && q + e < qend) dstk[q + e] = O::from(kc[q + e]);
+                    }
+                }
+                if constexpr (KV) {
+                    uint32_t *dstv = P.a_vals + (b - a0);
+                    for (uint32_t c = tid; c < (qend + 3) / 4; c += BT) {
+                        const uint32_t q = c * 4;
+                        if (q >= (uint32_t)a0 && q + 4 <= qend) {
+                            *reinterpret_cast<uint4 *>(dstv + q) = *reinterpret_cast<const uint4 *>(vc + q);
+                        } else {
+                            for (int e = 0; e < 4; ++e)
+                                if (q + e >= (uint32_t)a0 && q + e < qend) dstv[q + e] = vc[q + e];
+                        }
+                    }
+                }
+                if (tid == 0) {
+                    sh.s_base++;
+                    sh.s_bytes += 2ull * (sizeof(U) + (KV ? 4 : 0)) * m;
+                    sh.s_cyc_base += clock64() - sh.lc0;
+                    sh.lq[0] = sh.lq[1];
+                }
+                H::bsync();
+                continue;
             }
+            // slow path: the radix passes use kd / vd, so the next leaf's prefetch is dropped (after it
+            // lands) and issued again once this leaf's bulk stores have read kd / vd
+            if (sh.lq[1] != NONE) {
+                mbar_wait(bar, kphase);
+                kphase ^= 1u;
+            }
+            H::bsync();
+            radix_leaf(m, off, kmn, krange, vmn, vmx - vmn);
             fence_proxy_async();
             H::bsync();
-            {  // kd/vd[a0, a0 + m) -> A[b, b + m): 16-byte bodies by bulk stores, head/tail by threads
+            {  // kd/vd[off, off + m) -> A[b, b + m): 16-byte bodies by bulk stores, head/tail by threads
+                U *kd = kdk();
+                uint32_t *vd = kdv();
                 U *a = (U *)P.a_keys + b;
                 uint32_t *av = KV ? P.a_vals + b : nullptr;
-                int h = (4 - a0) & 3;
+                int h = (4 - off) & 3;
                 if (h > m) h = m;
                 const int nb = ((m - h) / 4) * 4;
                 if (tid > 0 && tid < 4 && tid - 1 < h) {
-                    a[tid - 1] = kd[a0 + tid - 1];
-                    if constexpr (KV) av[tid - 1] = vd[a0 + tid - 1];
+                    a[tid - 1] = kd[off + tid - 1];
+                    if constexpr (KV) av[tid - 1] = vd[off + tid - 1];
                 }
                 if (tid >= 4 && tid < 8 && h + nb + tid - 4 < m) {
-                    a[h + nb + tid - 4] = kd[a0 + h + nb + tid - 4];
-                    if constexpr (KV) av[h + nb + tid - 4] = vd[a0 + h + nb + tid - 4];
+                    a[h + nb + tid - 4] = kd[off + h + nb + tid - 4];
+                    if constexpr (KV) av[h + nb + tid - 4] = vd[off + h + nb + tid - 4];
                 }
                 if (tid == 0) {
                     if (nb) {
-                        bulk_s2g(a + h, kd + a0 + h, (unsigned)(nb * sizeof(U)));
-                        if constexpr (KV) bulk_s2g(av + h, vd + a0 + h, (unsigned)nb * 4u);
+                        bulk_s2g(a + h, kd + off + h, (unsigned)(nb * sizeof(U)));
+                        if constexpr (KV) bulk_s2g(av + h, vd + off + h, (unsigned)nb * 4u);
                     }
                     bulk_commit();
+                    if (sh.lq[1] != NONE) {
+                        bulk_wait_read();
+                        prefetch(P, sh.lq[1], bar);
+                    }
                     sh.s_base++;
                     sh.s_bytes += 2ull * (sizeof(U) + (KV ? 4 : 0)) * m;
-                    sh.s_cyc_base += clock64() - c0;
+                    sh.s_cyc_base += clock64() - sh.lc0;
+                    sh.lq[0] = sh.lq[1];
                 }
             }
-            cur = nxt;
-            k ^= 1;
+            H::bsync();
         }
         if (tid == 0) bulk_wait_all();
         H::bsync();
