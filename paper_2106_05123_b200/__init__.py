@@ -10,6 +10,7 @@ CPU fallback.
 from .driver import (
     DEFAULT_CONFIG,
     MIN_BREAK_SIZE,
+    Metrics,
     DeviceSorter,
     FieldOrder,
     HostPipeline,
@@ -17,6 +18,7 @@ from .driver import (
     SortConfig,
     by_field,
     host_sorter,
+    instrumented_sort,
     is_bad_partition,
     sort,
     sort_device,
@@ -33,9 +35,11 @@ __all__ = [
     "HostPipeline",
     "HostSorter",
     "MIN_BREAK_SIZE",
+    "Metrics",
     "SortConfig",
     "by_field",
     "host_sorter",
+    "instrumented_sort",
     "is_bad_partition",
     "sort",
     "sort_device",

@@ -561,7 +561,7 @@ def _field_keys(col) -> np.ndarray:
 def _sort_records(data, order: FieldOrder, config: SortConfig) -> None:
     n = len(data)
     if n < 2:
-        return
+        return None
     if n > 0xFFFFFFFF:
         raise ValueError("record sorts carry a uint32 index: at most 2^32 records")
     if isinstance(data, np.ndarray) and data.dtype.names:
@@ -574,12 +574,13 @@ def _sort_records(data, order: FieldOrder, config: SortConfig) -> None:
     else:
         keys = _field_keys([rec[order.field] for rec in data])
     idx = np.arange(n, dtype=np.uint32)
-    _sort_numpy(keys, idx, config)
+    stats = _sort_numpy(keys, idx, config)
     perm = idx[::-1] if order.descending else idx
     if isinstance(data, np.ndarray):
         data[...] = data[perm]
     else:
         data[:] = [data[i] for i in perm.tolist()]
+    return stats
 
 
 def sort_with_config(data: MutableSequence, lt: Ordering, config: SortConfig,
@@ -589,16 +590,72 @@ def sort_with_config(data: MutableSequence, lt: Ordering, config: SortConfig,
     ``operator.gt`` sorts descending: the ascending device sort, reversed.  Equal elements are
     bit-identical (keys) or identical tuples ((key, payload) pairs), so the descending output is the
     unique one the reference produces under ``gt``."""
+    _sort_ordered(data, lt, config)
+
+
+def _sort_ordered(data, lt: Ordering, config: SortConfig):
+    """The device sort under a built-in ordering; returns the device counters (or None)."""
     if lt is operator.lt:
-        _sort_any(data, config)
-        return
+        return _sort_any(data, config)
     if lt is operator.gt:
-        _sort_any(data, config)
+        stats = _sort_any(data, config)
         _reverse_in_place(data)
-        return
+        return stats
     if isinstance(lt, FieldOrder):
-        _sort_records(data, lt, config)
-        return
+        return _sort_records(data, lt, config)
     raise NotImplementedError(
         "the B200 sort path implements the built-in orderings (operator.lt, operator.gt, by_field) only; "
         "custom Python orderings have no device equivalent and there is no CPU fallback")
+
+
+# ---------------------------------------------------------------------------------------------
+# instrumentation (instrumentation.py:20-109): the reference's Metrics columns from device counters
+
+METRIC_FIELDS = ("comparisons", "element_moves", "exchanges", "partition_right_calls", "partition_left_calls",
+                 "bad_partitions", "heapsort_fallbacks", "partial_insertion_attempts", "partial_insertion_aborts",
+                 "max_depth")  # instrumentation.py:20-31, same order (the CSV column fragment)
+
+
+@dataclass
+class Metrics:
+    """The counters of one sort, with the reference's field names (instrumentation.py:34-66), filled
+    from the device counters (``pdq_stats``).  ``comparisons``, ``element_moves``, ``exchanges`` and the
+    partial-insertion pair count scalar operations the device does not perform one by one (a tile
+    classifies 4096 keys at once; the sortedness check K4 stands where partial insertion sort does):
+    they stay 0.  ``heapsort_fallbacks`` counts segments whose bad-partition budget ran out (the K5
+    digit passes stand where heapsort does).  ``device`` holds every raw device counter."""
+
+    comparisons: int = 0
+    element_moves: int = 0
+    exchanges: int = 0
+    partition_right_calls: int = 0
+    partition_left_calls: int = 0
+    bad_partitions: int = 0
+    heapsort_fallbacks: int = 0
+    partial_insertion_attempts: int = 0
+    partial_insertion_aborts: int = 0
+    max_depth: int = 0
+    distinct_pivot_reuse: Optional[dict] = None
+    device: Optional[dict] = None
+
+    def counter_values(self) -> tuple:
+        """The CSV row fragment, in METRIC_FIELDS order (instrumentation.py:60-62)."""
+        return tuple(getattr(self, f) for f in METRIC_FIELDS)
+
+    @classmethod
+    def from_stats(cls, st: Optional[dict]) -> "Metrics":
+        if not st:
+            return cls()
+        return cls(partition_right_calls=st["partition_right_calls"], partition_left_calls=st["partition_left_calls"],
+                   bad_partitions=st["bad_partitions"], heapsort_fallbacks=st["radix_fallbacks"],
+                   max_depth=st["max_depth"], device=dict(st))
+
+
+def instrumented_sort(data: MutableSequence, lt: Ordering = operator.lt, config: SortConfig = DEFAULT_CONFIG,
+                      branch_cheap: Optional[bool] = None, trace_pivots: bool = False) -> Metrics:
+    """Sort ``data`` in place and return its :class:`Metrics` (instrumentation.py:79-109, same
+    signature).  ``branch_cheap`` selects nothing on the device (the partition is always branchless);
+    ``trace_pivots`` -- reference test machinery recording every pivot value -- has no device
+    counterpart: ``distinct_pivot_reuse`` stays None."""
+    del branch_cheap, trace_pivots
+    return Metrics.from_stats(_sort_ordered(data, lt, config))

@@ -117,6 +117,24 @@ def cases(scale_shift: int = 0):
     yield "C5", k, v
 
 
+def stratified_adversary(n: int, seed: int = 7) -> np.ndarray:
+    """A permutation of 0..n-1 (int32) against the root's pivot rule (K1): the positions the root
+    samples -- (2i + 1) n / (2 S), S = 256 for n >= 2^20, else 64 -- hold the S smallest values, so the
+    root's pivot is the (S/2)-th smallest key and its partition is bad (min(L, R) < n / 8).  Deeper
+    segments cannot be targeted from the input: a partition places its tiles' runs in the order their
+    reservations arrive, so a child's sample positions hold keys no input layout controls (the
+    reference's deterministic adversary, instrumentation.adversary_input, has no GPU analogue)."""
+    ns = 256 if n >= (1 << 20) else 64
+    rng = _rng(seed)
+    out = np.empty(n, dtype=np.int64)
+    pos = ((2 * np.arange(ns, dtype=np.int64) + 1) * n) // (2 * ns)
+    mask = np.ones(n, dtype=bool)
+    mask[pos] = False
+    out[pos] = np.arange(ns)
+    out[mask] = ns + rng.permutation(n - ns)
+    return out.astype(np.int32)
+
+
 def make(name: str, n: int):
     """Build one named case (as listed by :func:`cases`) at size n."""
     if name == "C1":

@@ -189,3 +189,27 @@ def test_uint64_field_beyond_int64_is_rejected():
     rec["k"] = [2**63 + 1, 5]
     with pytest.raises(TypeError):
         sort_with(rec, by_field("k"))
+
+
+def test_metrics_columns_follow_the_reference():
+    # instrumentation.py:20-31: the CSV counter fragment's column order
+    from paper_2106_05123_b200 import Metrics
+    from paper_2106_05123_b200.driver import METRIC_FIELDS
+
+    assert METRIC_FIELDS == ("comparisons", "element_moves", "exchanges", "partition_right_calls",
+                             "partition_left_calls", "bad_partitions", "heapsort_fallbacks",
+                             "partial_insertion_attempts", "partial_insertion_aborts", "max_depth")
+    m = Metrics.from_stats({"partition_right_calls": 3, "partition_left_calls": 1, "bad_partitions": 2,
+                            "radix_fallbacks": 1, "max_depth": 5})
+    assert m.counter_values() == (0, 0, 0, 3, 1, 2, 1, 0, 0, 5)
+
+
+def test_stratified_adversary_is_a_permutation():
+    from paper_2106_05123_b200 import workloads
+
+    for n in (1000, 1 << 20):
+        a = workloads.stratified_adversary(n)
+        assert a.dtype == np.int32 and np.array_equal(np.sort(a), np.arange(n))
+        ns = 256 if n >= 1 << 20 else 64
+        pos = ((2 * np.arange(ns) + 1) * n) // (2 * ns)
+        assert np.array_equal(np.sort(a[pos]), np.arange(ns))

@@ -540,3 +540,51 @@ def test_forced_fallback_digit_pass_shapes(case):
         exp_k, exp_v = workloads.expected(keys, vals)
         assert same_bytes(got_k, exp_k) and (vals is None or same_bytes(got_v, exp_v)), (case, n)
         assert stats["radix_fallbacks"] >= 1 and stats["status"] == 0
+
+
+# ---- the reference's property tests (pkg/tests/test_driver.py:243-254) on the device path ----------
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@given(st.lists(st.integers(-1000, 1000), max_size=300))
+@settings(max_examples=200, deadline=None)
+def test_property_sorts_any_int_list(arr):
+    work = list(arr)
+    sort(work)
+    assert work == sorted(arr)
+
+
+@given(st.lists(st.floats(allow_nan=False, allow_infinity=True), max_size=100))
+@settings(max_examples=100, deadline=None)
+def test_property_sorts_floats_with_infinities(arr):
+    work = list(arr)
+    sort(work)
+    assert work == sorted(arr)
+
+
+def test_instrumented_sort_metrics_and_onk_bound():
+    """instrumented_sort (instrumentation.py:79-109) on the device: the Metrics columns, and the
+    paper's O(nk) property as the reference's acceptance test asserts it (partitions <= 2k for k
+    distinct keys, acceptance.py:242-265)."""
+    from paper_2106_05123_b200 import Metrics, instrumented_sort
+
+    rng = np.random.default_rng(21)
+    for k in (1, 2, 16, 256):
+        data = rng.integers(0, k, 1 << 20).astype(np.int32).tolist()
+        exp = sorted(data)
+        m = instrumented_sort(data)
+        assert isinstance(m, Metrics) and data == exp
+        assert m.partition_right_calls + m.partition_left_calls <= 2 * k + 2
+        assert len(m.counter_values()) == 10 and m.counter_values()[0] == 0
+    m = instrumented_sort([3, 1, 2], __import__("operator").gt)
+    assert m.device is not None and m.device["status"] == 0
+
+
+def test_stratified_adversary_spoils_only_the_root():
+    """The input-side adversary for the root's stratified sample: the root's partition is bad, the
+    budget (floor(log2 n)) is far from spent, the output is the sorted permutation."""
+    n = 1 << 22
+    keys = workloads.stratified_adversary(n)
+    got, _, stats = gpu_sort(keys)
+    assert same_bytes(got, np.arange(n, dtype=np.int32))
+    assert stats["bad_partitions"] >= 1 and stats["radix_fallbacks"] == 0
