@@ -67,7 +67,9 @@ typedef struct pdq_config {
     int32_t bad_budget;               /* -1: floor(log2 n) (driver.py:263); >= 0 overrides (0 forces the
                                          radix fallback on the first big segment: test knob) */
     int32_t reserved[4];              /* reserved[0] > 0: profiling knob, stop descending at that
-                                         depth (output NOT sorted); keep 0 */
+                                         depth (output NOT sorted); keep 0.
+                                         reserved[1] > 0: smallest n for K4's two-run path (default 2^18;
+                                         tests lower it) */
 } pdq_config;
 
 /* Device counters (the GPU analogue of Metrics, instrumentation.py:20-61). */
@@ -81,7 +83,10 @@ typedef struct pdq_stats {
     int64_t tiles;                  /* partition tiles processed */
     int64_t bytes_algorithmic;      /* SURVEY.md §8(d) byte model over the init + sorter kernels, summed
                                        over the segments they actually processed */
-    int64_t check_result;           /* K4: bit0 a descent seen, bit1 an ascent seen */
+    int64_t check_result;           /* K4: bit0 a descent seen, bit1 an ascent seen, bit2 a descent in the
+                                       first half (the pass may then stop early); bits 4-5: the two-run path
+                                       was taken and the second run was 1 ascending, 2 descending (reversed
+                                       in place), 3 sorted by the partition tree */
     int64_t segments;               /* descriptors allocated */
     int64_t status;                 /* 0 or a negative pdq_status */
     int64_t bytes_check;            /* bytes the K4 check kernel read */
@@ -96,6 +101,8 @@ typedef struct pdq_stats {
     int64_t bytes_base;             /* algorithmic bytes of the K7 base-case kernel (not in bytes_algorithmic) */
     int64_t sort_ns;                /* device-timer span of the persistent sorter (first CTA start -> last end) */
     int64_t base_ns;                /*   ... of the base-case kernel (0 if it did not run) */
+    int64_t run_split;              /* K4 two-run path: A[0, run_split) was a sorted prefix merged with the
+                                       rest (0: path not taken); the merge's bytes are in bytes_base */
 } pdq_stats;
 
 /* Fill `cfg` with the reference defaults (driver.py:55-63) and GPU defaults. */

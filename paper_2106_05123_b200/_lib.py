@@ -92,6 +92,7 @@ STAT_FIELDS = (
     "bytes_base",
     "sort_ns",
     "base_ns",
+    "run_split",
 )
 
 

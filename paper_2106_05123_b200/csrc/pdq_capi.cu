@@ -63,6 +63,9 @@ constexpr int MIN_BASE = 1024;
 #ifndef PDQ_CHUNK_MAX
 #define PDQ_CHUNK_MAX 32  // tiles per ring task at most
 #endif
+#ifndef PDQ_RUNS_MIN
+#define PDQ_RUNS_MIN (1 << 18)  // K4 takes the two-run path (sorted prefix of >= n/2 + merge) from this size
+#endif
 #ifndef PDQ_CHUNK_DIV
 #define PDQ_CHUNK_DIV 2  // the root level gets about this many tasks per CTA
 #endif
@@ -324,6 +327,7 @@ extern "C" int pdq_sort_timed(void *keys, int dtype, uint32_t *payload, int64_t 
     P.base_size = cfg.base_case_size;
     P.budget0 = cfg.bad_budget;
     P.debug_depth = cfg.reserved[0];
+    P.runs_min = cfg.reserved[1] > 0 ? (int64_t)cfg.reserved[1] : (int64_t)PDQ_RUNS_MIN;
     P.leaves = (uint64_t *)(ws + L.leaves);
     P.leaf_cap = L.leaf_cap;
     P.rslots = (unsigned long long *)(ws + L.rslots);
@@ -362,7 +366,8 @@ extern "C" int pdq_sort_finish(void *workspace, pdq_stats *out, void *stream) {
         out->max_depth = (int64_t)st.c_max_depth;
         out->tiles = (int64_t)st.c_tiles;
         out->bytes_algorithmic = (int64_t)st.c_bytes;
-        out->check_result = (int64_t)st.check_bits;
+        out->check_result = (int64_t)(st.check_bits | st.run_kind << 4);
+        out->run_split = (int64_t)st.run_split;
         out->segments = (int64_t)st.seg_alloc;
         out->status = (int64_t)st.status;
         out->bytes_check = (int64_t)st.c_bytes_check;

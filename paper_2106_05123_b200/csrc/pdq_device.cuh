@@ -87,7 +87,14 @@ struct __align__(128) State {
     unsigned int check_bits;       // K4: 1 descent seen, 2 ascent seen
     unsigned int reverse;          // K4 decided the input is non-increasing
     unsigned int rslot_alloc;      // K5 radix-slot bump allocator
-    unsigned long long pad_d[12];
+    // K4 run detection (exact whenever the check pass was not cut short): the smallest descent index
+    // (stored inverted: a zeroed state and atomicMax give the minimum), the largest descent index + 1
+    // and the largest ascent index + 1
+    unsigned long long run_d1_inv, run_dl, run_la;
+    unsigned long long run_split;  // > 0: A[0, run_split) and A[run_split, n) are merged after the sort
+    unsigned int run_kind;         // the second run was 1 ascending, 2 descending (reversed), 3 sorted by the tree
+    unsigned int gbar;             // grid barrier of the leaf kernel's merge epilogue
+    unsigned long long pad_d[7];
     // counters (pdq_stats order)
     unsigned long long leaf_count;  // queued base-case segments (K7 kernel input)
     unsigned long long leaf_next;   // K7 kernel claim counter
@@ -119,6 +126,7 @@ struct Params {
     int base_size;
     int budget0;
     int debug_depth;   // > 0: segments at this depth are dropped unsorted (profiling only)
+    int64_t runs_min;  // K4 merges two runs only for n >= runs_min
     uint64_t *leaves;  // queued leaves: begin << 16 | (size - 1) << 1 | in-B
     unsigned long long leaf_cap;
     uint32_t chunk;    // tiles per ring task

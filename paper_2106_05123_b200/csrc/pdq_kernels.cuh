@@ -1715,11 +1715,18 @@ struct Sorter {
 };
 
 // ---- K4: adjacent-compare reduction with early exit ---------------------------------------------
+// One pass over adjacent pairs: bit 0 a descent was seen, bit 1 an ascent, bit 2 a descent in the first
+// half of the array (or anywhere, for arrays too short for the two-run path).  The pass is cut short
+// once bits 1 and 2 are both set: the input is then neither sorted, nor reversed, nor a sorted prefix of
+// at least half the array followed by a second run.  When it runs to the end, the first and last descent
+// and the last ascent are exact (k_init reads them to recognise two runs: small_sorts.py:76-115's
+// "nearly sorted" case on the GPU is a sorted prefix followed by anything).
 template <class U, bool FLOAT, bool KV>
 __global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Params P) {
     using O = Ord<U, FLOAT>;
-    __shared__ unsigned s_stop;
-    const int tid = threadIdx.x;
+    __shared__ unsigned s_pub;
+    __shared__ unsigned long long s_red[3][WARPS];
+    const int tid = threadIdx.x, lane = tid & 31;
     pdl_trigger();  // k_init (one CTA) may be scheduled now; it waits for this grid before reading
     {  // the task ring starts empty (all-ones words match no round tag); k_init pushes after this grid
         uint4 *r4 = reinterpret_cast<uint4 *>(P.ring);
@@ -1727,41 +1734,129 @@ __global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Param
         for (int64_t i = (int64_t)blockIdx.x * THREADS + tid; i < words; i += (int64_t)gridDim.x * THREADS)
             r4[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
     }
+    if (tid == 0) s_pub = 0;
+    __syncthreads();
     const U *a = (const U *)P.a_keys;
     const int64_t n = P.n;
+    constexpr int E = 4, STEPS = ITEMS / E;  // a thread reads 4 elements (16-byte vectors) per step
     const int64_t CH = (int64_t)THREADS * ITEMS;
+    // a descent at index i < early leaves a sorted prefix shorter than half the array
+    const int64_t early = n >= P.runs_min ? (n + 1) / 2 - 1 : n;
+    constexpr unsigned long long NONE = ~0ull;
+    unsigned long long d1 = NONE, dl = 0, la = 0;  // this thread's first descent, last descent + 1, last ascent + 1
     unsigned long long bytes = 0;
     for (int64_t c0 = (int64_t)blockIdx.x * CH; c0 < n - 1; c0 += (int64_t)gridDim.x * CH) {
-        if (tid == 0) s_stop = (ld_volatile_u32(&P.st->check_bits) == 3u);
-        __syncthreads();
-        if (s_stop) break;
+        // the verdict so far (its latency overlaps the chunk's loads; threads may leave one chunk apart)
+        const unsigned flag = ld_volatile_u32(&P.st->check_bits);
         unsigned bits = 0;
-        // each thread compares ITEMS pairs; lanes read adjacent elements (coalesced per slot)
-#pragma unroll 4
-        for (int j = 0; j < ITEMS; ++j) {
-            const int64_t i = c0 + (int64_t)j * THREADS + tid;
-            if (i < n - 1) {
-                const uint64_t x = (uint64_t)O::to(a[i]), y = (uint64_t)O::to(a[i + 1]);
-                const uint32_t xv = KV ? P.a_vals[i] : 0u, yv = KV ? P.a_vals[i + 1] : 0u;
-                bits |= pless<KV>(y, yv, x, xv) ? 1u : 0u;
-                bits |= pless<KV>(x, xv, y, yv) ? 2u : 0u;
+#pragma unroll
+        for (int st = 0; st < STEPS; ++st) {
+            const int64_t i = c0 + ((int64_t)st * THREADS + tid) * E;
+            U k[E + 1];
+            uint32_t v[E + 1];
+#pragma unroll
+            for (int q = 0; q <= E; ++q) {
+                k[q] = 0;
+                v[q] = 0;
+            }
+            if (i + E <= n) {
+                if constexpr (sizeof(U) == 4) {
+                    const uint4 y = __ldg(reinterpret_cast<const uint4 *>(a + i));
+                    k[0] = (U)y.x; k[1] = (U)y.y; k[2] = (U)y.z; k[3] = (U)y.w;
+                } else {
+                    const ulonglong2 y0 = __ldg(reinterpret_cast<const ulonglong2 *>(a + i));
+                    const ulonglong2 y1 = __ldg(reinterpret_cast<const ulonglong2 *>(a + i + 2));
+                    k[0] = (U)y0.x; k[1] = (U)y0.y; k[2] = (U)y1.x; k[3] = (U)y1.y;
+                }
+                if constexpr (KV) {
+                    const uint4 z = __ldg(reinterpret_cast<const uint4 *>(P.a_vals + i));
+                    v[0] = z.x; v[1] = z.y; v[2] = z.z; v[3] = z.w;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < E; ++q)
+                    if (i + q < n) {
+                        k[q] = a[i + q];
+                        if constexpr (KV) v[q] = P.a_vals[i + q];
+                    }
+            }
+            // the element after this thread's vector: the next lane's first (lane 31 loads it)
+            if constexpr (sizeof(U) == 4) k[E] = (U)__shfl_down_sync(0xffffffffu, (uint32_t)k[0], 1);
+            else k[E] = (U)__shfl_down_sync(0xffffffffu, (unsigned long long)k[0], 1);
+            if constexpr (KV) v[E] = __shfl_down_sync(0xffffffffu, v[0], 1);
+            if (lane == 31 && i + E < n) {
+                k[E] = a[i + E];
+                if constexpr (KV) v[E] = P.a_vals[i + E];
+            }
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                if (i + q < n - 1) {
+                    const uint64_t x = (uint64_t)O::to(k[q]), y = (uint64_t)O::to(k[q + 1]);
+                    if (pless<KV>(y, v[q + 1], x, v[q])) {  // (a thread's indices only grow)
+                        bits |= i + q < early ? 5u : 1u;
+                        if (d1 == NONE) d1 = (unsigned long long)(i + q);
+                        dl = (unsigned long long)(i + q) + 1;
+                    }
+                    if (pless<KV>(x, v[q], y, v[q + 1])) {
+                        bits |= 2u;
+                        la = (unsigned long long)(i + q) + 1;
+                    }
+                }
             }
         }
         bits = __reduce_or_sync(0xffffffffu, bits);
-        if ((tid & 31) == 0 && bits) atomicOr(&P.st->check_bits, bits);
-        const int64_t hi = c0 + CH < n ? c0 + CH : n;
-        bytes += (unsigned long long)(hi - c0) * (sizeof(U) + (KV ? 4 : 0));
-        __syncthreads();
+        // publish only what neither this CTA nor anyone else has published yet: thousands of atomics on
+        // one word serialise in its L2 slice (8 per CTA x 1184 CTAs cost ~25 us at the start of every sort)
+        if (lane == 0 && bits) {
+            const unsigned fresh = bits & ~atomicOr(&s_pub, bits);
+            if (fresh && (fresh & ~ld_volatile_u32(&P.st->check_bits))) atomicOr(&P.st->check_bits, fresh);
+        }
+        if (tid == 0) {
+            const int64_t hi = c0 + CH < n ? c0 + CH : n;
+            bytes += (unsigned long long)(hi - c0) * (sizeof(U) + (KV ? 4 : 0));
+        }
+        if ((flag & 6u) == 6u) break;
     }
-    if (tid == 0 && bytes) atomicAdd(&P.st->c_bytes_check, bytes);
+    // CTA reduction of the run marks, one atomic each
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a1 = __shfl_xor_sync(0xffffffffu, d1, o), a2 = __shfl_xor_sync(0xffffffffu, dl, o),
+                                 a3 = __shfl_xor_sync(0xffffffffu, la, o);
+        d1 = a1 < d1 ? a1 : d1;
+        dl = a2 > dl ? a2 : dl;
+        la = a3 > la ? a3 : la;
+    }
+    if (lane == 0) {
+        s_red[0][tid >> 5] = d1;
+        s_red[1][tid >> 5] = dl;
+        s_red[2][tid >> 5] = la;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < WARPS; ++w) {
+            d1 = s_red[0][w] < d1 ? s_red[0][w] : d1;
+            dl = s_red[1][w] > dl ? s_red[1][w] : dl;
+            la = s_red[2][w] > la ? s_red[2][w] : la;
+        }
+        if (d1 != NONE) atomicMax(&P.st->run_d1_inv, ~d1);
+        if (dl) atomicMax(&P.st->run_dl, dl);
+        if (la) atomicMax(&P.st->run_la, la);
+        if (bytes) atomicAdd(&P.st->c_bytes_check, bytes);
+    }
 }
 
 // ---- init: decide from K4, reverse flag, root segment --------------------------------------------
+// K4 verdicts: no descent -> sorted; no ascent -> reversed in place; no descent in the first half (the
+// pass then ran to the end) -> two runs: A[0, s) is sorted, s = first descent + 1 >= n / 2, and the rest
+// is left as it is (ascending: a single descent), reversed (no ascent beyond s) or sorted by the tree as
+// the root segment [s, n); the leaf kernel then merges the two runs (RunsMerge).  Anything else: the
+// root segment is the whole array.
 template <class U, bool FLOAT, bool KV>
 __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params P) {
     using S = Sorter<U, FLOAT, KV>;
     Shared &sh = g_sh;
     __shared__ int s_action;
+    __shared__ long long s_root;
     const int tid = threadIdx.x;
     pdl_wait();     // k_check's verdict
     pdl_trigger();  // the sorter's CTAs may be scheduled; they wait for this grid before reading
@@ -1769,10 +1864,27 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
         S::zero_counters();
         const unsigned bits = P.st->check_bits;
         int action = 0;  // 0 = sort, 1 = done (sorted), 2 = reverse
+        long long root = 0;
         if (P.n <= 1) action = 1;
         else if (P.use_check && !(bits & 1u)) action = 1;
         else if (P.use_check && !(bits & 2u)) action = 2;
+        else if (P.use_check && !(bits & 4u) && P.n >= P.runs_min) {
+            const unsigned long long s = ~P.st->run_d1_inv + 1;  // the second run starts here
+            P.st->run_split = s;
+            if (P.st->run_dl == s) {  // a single descent: the second run is ascending
+                P.st->run_kind = 1;
+                action = 1;
+            } else if (P.st->run_la <= s) {  // no ascent beyond s: the second run is reversed in place
+                P.st->run_kind = 2;
+                action = 2;
+            } else {  // the tree sorts [s, n)
+                P.st->run_kind = 3;
+                root = (long long)s;
+                P.st->keys_final = s;
+            }
+        }
         s_action = action;
+        s_root = root;
         if (action == 1) {
             P.st->keys_final = P.n;
             P.st->done = 1;
@@ -1780,15 +1892,16 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
             P.st->reverse = 1;
             P.st->keys_final = P.n;
             P.st->done = 1;
-            sh.s_bytes += 2ull * (sizeof(U) + (KV ? 4 : 0)) * (unsigned long long)P.n;
+            sh.s_bytes += 2ull * (sizeof(U) + (KV ? 4 : 0)) * (unsigned long long)(P.n - (int64_t)P.st->run_split);
         }
     }
     __syncthreads();
     if (s_action == 0) {
+        const int64_t m = P.n - s_root;
         int budget = P.budget0;
-        if (budget < 0) budget = 63 - __clzll((long long)P.n);  // driver.py:263: n.bit_length() - 1
+        if (budget < 0) budget = 63 - __clzll((long long)m);  // driver.py:263: n.bit_length() - 1
         typename S::Bnd none{};
-        S::spawn(P, 0, P.n, false, none, budget, 0, false, -1);
+        S::spawn(P, s_root, P.n, false, none, budget, 0, false, -1);
     }
     __syncthreads();
     if (tid == 0) S::flush_counters(P);
@@ -2904,18 +3017,243 @@ struct WideLeaf {
     }
 };
 
+// ---- K4 two-run epilogue: merge A[0, s) and A[s, n) (both ascending) -----------------------------------
+// Runs in the leaf kernel's persistent CTAs (one 1024-thread CTA per SM, all resident) after the leaves:
+// grid barrier, merge-path tiles A -> B, grid barrier, copy B -> A.  A tile is T = 8192 outputs: its two
+// input ranges come from a merge-path search over global memory (every thread of a CTA searches one of
+// the CTA's tile boundaries, all at once), land in shared memory as ordered images, and every thread
+// merges V = 8 consecutive outputs from its own diagonal and stores them as 16-byte vectors.  Ties take
+// the first run's element (for keys-only sorts equal keys are identical bits; with a payload the order
+// is the (key, payload) order, so there are no ties between distinct elements).
+template <class U, bool FLOAT, bool KV>
+struct RunsMerge {
+    using O = Ord<U, FLOAT>;
+    static constexpr int BT = 1024, V = 8, T = BT * V, BATCH = 1024;
+    // two stages of raw keys (+ payloads): tile k + 1 arrives by cp.async while tile k is merged
+    static constexpr int VIN = T * (int)sizeof(U), STAGE = VIN + (KV ? T * 4 : 0), BND = 2 * STAGE;
+    __host__ __device__ static constexpr int bytes() { return BND + (BATCH + 1) * 8; }
+    __device__ __forceinline__ static U *kin(int st) { return reinterpret_cast<U *>(g_dsm + st * STAGE); }
+    __device__ __forceinline__ static uint32_t *vin(int st) {
+        return reinterpret_cast<uint32_t *>(g_dsm + st * STAGE + VIN);
+    }
+    __device__ __forceinline__ static int64_t *bnd() { return reinterpret_cast<int64_t *>(g_dsm + BND); }
+    template <class E>
+    __device__ __forceinline__ static void cp_async(E *sdst, const E *gsrc) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_addr(sdst)), "l"(gsrc), "n"((int)sizeof(E))
+                     : "memory");
+    }
+    __device__ __forceinline__ static void bsync() { asm volatile("bar.sync 1, %0;" ::"n"(BT) : "memory"); }
+
+    __device__ static void grid_barrier(const Params &P, unsigned &round) {
+        bsync();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(&P.st->gbar, 1u);
+            const unsigned target = (++round) * gridDim.x;
+            while (ld_volatile_u32(&P.st->gbar) < target) __nanosleep(128);
+            __threadfence();
+        }
+        bsync();
+    }
+
+    // Warp-cooperative 32-ary search: the first x in [lo, hi] with pred(x) false (pred is true below it,
+    // false from it on; evaluated on [lo, hi) only).  Five rounds of 32 probes cover 2^25 positions, each
+    // round one memory latency.
+    template <class F>
+    __device__ __forceinline__ static int64_t warp_first_false(int64_t lo, int64_t hi, F pred) {
+        const int lane = threadIdx.x & 31;
+        while (lo < hi) {
+            const int64_t step = (hi - lo + 31) / 32;
+            const int64_t p = lo + lane * step;
+            const bool t = p < hi && pred(p);
+            const int c = __popc(__ballot_sync(0xffffffffu, t));  // probes 0 .. c-1 are true
+            if (c == 0) return lo;
+            const int64_t nhi = lo + (int64_t)c * step;
+            lo += (int64_t)(c - 1) * step + 1;
+            hi = nhi < hi ? nhi : hi;
+        }
+        return lo;
+    }
+    __device__ __forceinline__ static uint64_t keyat(const Params &P, int64_t i) {
+        return (uint64_t)O::to(ldcg((const U *)P.a_keys + i));
+    }
+    __device__ __forceinline__ static uint32_t valat(const Params &P, int64_t i) {
+        return KV ? ldcg(P.a_vals + i) : 0u;
+    }
+
+    __device__ static void run(const Params &P) {
+        Shared &sh = g_sh;
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        const int64_t n = P.n, s = (int64_t)P.st->run_split;
+        const U *a = (const U *)P.a_keys;
+        U *b = (U *)P.b_keys;
+        int64_t *bd = bnd();
+        unsigned round = 0;
+        grid_barrier(P, round);  // every leaf is in A
+        // The window that changes: first-run elements <= the second run's smallest stay where they are, and
+        // so do second-run elements >= the first run's largest (appending slightly newer keys to a sorted
+        // array merges only the overlap).  The window starts at a multiple of 8 elements (16-byte stores).
+        if (warp == 0) {
+            const uint64_t y = keyat(P, s);
+            const uint32_t yv = valat(P, s);
+            const int64_t p0 = warp_first_false(0, s, [&](int64_t i) { return !pless<KV>(y, yv, keyat(P, i), valat(P, i)); });
+            if (lane == 0) bd[0] = p0 & ~(int64_t)7;
+        } else if (warp == 1) {
+            const uint64_t x = keyat(P, s - 1);
+            const uint32_t xv = valat(P, s - 1);
+            const int64_t q = warp_first_false(0, n - s, [&](int64_t j) { return pless<KV>(keyat(P, s + j), valat(P, s + j), x, xv); });
+            if (lane == 0) bd[1] = s + q;
+        }
+        bsync();
+        const int64_t o0 = bd[0], r2e = bd[1];
+        const int64_t len1 = s - o0, len2 = r2e - s, m = len1 + len2;
+        bsync();
+        const int64_t ntiles = (m + T - 1) / T;
+        const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;  // consecutive tiles of this CTA
+        const int64_t t_lo = (int64_t)blockIdx.x * per, t_hi = t_lo + per < ntiles ? t_lo + per : ntiles;
+        unsigned long long moved = 0;
+        for (int64_t tb = t_lo; tb < t_hi; tb += BATCH) {
+            const int64_t nb = t_hi - tb < BATCH ? t_hi - tb : BATCH;
+            bsync();
+            // merge path: first-run elements among the first d outputs, one boundary per warp at a time
+            for (int64_t k = warp; k <= nb; k += BT / 32) {
+                const int64_t d = (tb + k) * T < m ? (tb + k) * T : m;
+                const int64_t lo = d > len2 ? d - len2 : 0, hi = d < len1 ? d : len1;
+                const int64_t r = warp_first_false(lo, hi, [&](int64_t mid) {
+                    return !pless<KV>(keyat(P, s + (d - 1 - mid)), valat(P, s + (d - 1 - mid)), keyat(P, o0 + mid),
+                                      valat(P, o0 + mid));
+                });
+                if (lane == 0) bd[k] = r;
+            }
+            bsync();
+            // tile k's two input ranges -> stage k & 1 (raw bits; the ordered image is taken on read)
+            auto issue = [&](int64_t k) {
+                const int64_t d0 = (tb + k) * T, d1 = d0 + T < m ? d0 + T : m;
+                const int64_t i0 = bd[k], j0 = d0 - i0;
+                const int L1 = (int)(bd[k + 1] - i0), L = (int)(d1 - d0);
+                U *kd = kin((int)(k & 1));
+                uint32_t *vd = vin((int)(k & 1));
+                for (int x = tid; x < L; x += BT) {
+                    const int64_t src = x < L1 ? o0 + i0 + x : s + j0 + (x - L1);
+                    cp_async(kd + x, a + src);
+                    if constexpr (KV) cp_async(vd + x, P.a_vals + src);
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            };
+            issue(0);
+            for (int64_t k = 0; k < nb; ++k) {
+                const int64_t d0 = (tb + k) * T, d1 = d0 + T < m ? d0 + T : m;
+                const int64_t i0 = bd[k], i1 = bd[k + 1];
+                const int L1 = (int)(i1 - i0), L = (int)(d1 - d0), L2 = L - L1;
+                if (k + 1 < nb) {
+                    issue(k + 1);
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");
+                } else {
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                }
+                bsync();
+                const U *kr = kin((int)(k & 1));
+                const uint32_t *vi = vin((int)(k & 1));
+                auto ki = [&](int idx) -> U { return O::to(kr[idx]); };
+                const int dl = tid * V < L ? tid * V : L;
+                int lo = dl > L2 ? dl - L2 : 0, hi = dl < L1 ? dl : L1;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    const uint64_t x = (uint64_t)ki(mid), y = (uint64_t)ki(L1 + dl - 1 - mid);
+                    const uint32_t xv = KV ? vi[mid] : 0u, yv = KV ? vi[L1 + dl - 1 - mid] : 0u;
+                    if (!pless<KV>(y, yv, x, xv)) lo = mid + 1;
+                    else hi = mid;
+                }
+                int ia = lo, ib = dl - lo;
+                U ok[V];
+                uint32_t ov[V];
+                U xa = ia < L1 ? ki(ia) : (U)0, xb = ib < L2 ? ki(L1 + ib) : (U)0;
+                uint32_t va = (KV && ia < L1) ? vi[ia] : 0u, vb = (KV && ib < L2) ? vi[L1 + ib] : 0u;
+#pragma unroll
+                for (int q = 0; q < V; ++q) {
+                    const bool takeA = ib >= L2 || (ia < L1 && !pless<KV>((uint64_t)xb, vb, (uint64_t)xa, va));
+                    ok[q] = O::from(takeA ? xa : xb);
+                    ov[q] = takeA ? va : vb;
+                    if (takeA) {
+                        ++ia;
+                        xa = ia < L1 ? ki(ia) : (U)0;
+                        if constexpr (KV) va = ia < L1 ? vi[ia] : 0u;
+                    } else {
+                        ++ib;
+                        xb = ib < L2 ? ki(L1 + ib) : (U)0;
+                        if constexpr (KV) vb = ib < L2 ? vi[L1 + ib] : 0u;
+                    }
+                }
+                U *dst = b + o0 + d0 + dl;
+                if (dl + V <= L) {  // o0 + d0 + dl is a multiple of 8 elements: 16-byte aligned vectors
+                    constexpr int KPV = 16 / (int)sizeof(U);
+#pragma unroll
+                    for (int q = 0; q < V / KPV; ++q) {
+                        union {
+                            U t[KPV];
+                            uint4 u;
+                        } pk;
+#pragma unroll
+                        for (int e = 0; e < KPV; ++e) pk.t[e] = ok[q * KPV + e];
+                        reinterpret_cast<uint4 *>(dst)[q] = pk.u;
+                    }
+                    if constexpr (KV) {
+                        uint4 *dv = reinterpret_cast<uint4 *>(P.b_vals + o0 + d0 + dl);
+                        dv[0] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+                        dv[1] = make_uint4(ov[4], ov[5], ov[6], ov[7]);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < V; ++q)
+                        if (dl + q < L) {
+                            dst[q] = ok[q];
+                            if constexpr (KV) P.b_vals[o0 + d0 + dl + q] = ov[q];
+                        }
+                }
+                moved += (tid == 0) ? (unsigned long long)L : 0ull;
+                bsync();
+            }
+        }
+        grid_barrier(P, round);  // B holds the merged array
+        {  // copy the window back, 16-byte vectors (o0 is a multiple of 8 elements)
+            constexpr int KPV = 16 / (int)sizeof(U);
+            const int64_t gt = (int64_t)blockIdx.x * BT + tid, gs = (int64_t)gridDim.x * BT;
+            const int64_t nv = m / KPV;
+            const uint4 *src = reinterpret_cast<const uint4 *>(b + o0);
+            uint4 *dst = reinterpret_cast<uint4 *>((U *)P.a_keys + o0);
+            for (int64_t c = gt; c < nv; c += gs) dst[c] = __ldcg(src + c);
+            for (int64_t i = o0 + nv * KPV + gt; i < r2e; i += gs) ((U *)P.a_keys)[i] = b[i];
+            if constexpr (KV) {
+                const int64_t nw = m / 4;
+                const uint4 *sv = reinterpret_cast<const uint4 *>(P.b_vals + o0);
+                uint4 *dv = reinterpret_cast<uint4 *>(P.a_vals + o0);
+                for (int64_t c = gt; c < nw; c += gs) dv[c] = __ldcg(sv + c);
+                for (int64_t i = o0 + nw * 4 + gt; i < r2e; i += gs) P.a_vals[i] = P.b_vals[i];
+            }
+        }
+        // merge + copy: 4 (w + p) bytes per element (SURVEY.md §8(d) counts a pass as read + write)
+        if (tid == 0) sh.s_bytes += 4ull * (sizeof(U) + (KV ? 4 : 0)) * moved;
+    }
+};
+
 template <class U, bool FLOAT, bool KV>
 __global__ void __launch_bounds__(1024, 1) k_base_wide(const __grid_constant__ Params P) {
     using S = Sorter<U, FLOAT, KV>;
     Shared &sh = g_sh;
     const int tid = threadIdx.x;
     pdl_wait();  // the sorter's leaf queue
-    if (ld_volatile_u32(&P.st->reverse)) return;
+    const bool runs = P.st->run_split != 0;
+    const bool rev = ld_volatile_u32(&P.st->reverse) != 0;
+    if (rev && !runs) return;
     if (tid == 0) {
         S::zero_counters();
         atomicMax(&P.st->t_base_b_inv, ~globaltimer_ns());
     }
-    WideLeaf<U, FLOAT, KV>::run(P);
+    if (!rev) WideLeaf<U, FLOAT, KV>::run(P);
+    if (runs) {
+        static_assert(RunsMerge<U, FLOAT, KV>::bytes() <= WideLeaf<U, FLOAT, KV>::bytes(), "merge tiles fit the leaf buffers");
+        RunsMerge<U, FLOAT, KV>::run(P);
+    }
     if (tid == 0) {
         atomicMax(&P.st->t_base_e, globaltimer_ns());
         atomicAdd(&P.st->c_bytes_base, sh.s_bytes);
@@ -2930,12 +3268,18 @@ __global__ void __launch_bounds__(BigLeaf<FLOAT>::BT, 1) k_base_big(const __grid
     Shared &sh = g_sh;
     const int tid = threadIdx.x;
     pdl_wait();  // the sorter's leaf queue
-    if (ld_volatile_u32(&P.st->reverse)) return;
+    const bool runs = P.st->run_split != 0;
+    const bool rev = ld_volatile_u32(&P.st->reverse) != 0;
+    if (rev && !runs) return;
     if (tid == 0) {
         S::zero_counters();
         atomicMax(&P.st->t_base_b_inv, ~globaltimer_ns());
     }
-    BigLeaf<FLOAT>::run(P);
+    if (!rev) BigLeaf<FLOAT>::run(P);
+    if (runs) {
+        static_assert(RunsMerge<uint32_t, FLOAT, false>::bytes() <= BigLeaf<FLOAT>::bytes(), "merge tiles fit the leaf buffers");
+        RunsMerge<uint32_t, FLOAT, false>::run(P);
+    }
     if (tid == 0) {
         atomicMax(&P.st->t_base_e, globaltimer_ns());
         atomicAdd(&P.st->c_bytes_base, sh.s_bytes);
@@ -2963,14 +3307,17 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
     pdl_wait();  // k_init's root segment and verdict
     if (tid == 0) atomicMax(&P.st->t_sort_b_inv, ~globaltimer_ns());
 
-    // K4 reverse: a non-increasing input is reversed in place (one read + one write pass)
+    // K4 reverse: a non-increasing input (or second run, [run_split, n)) is reversed in place (one read +
+    // one write pass)
     if (ld_volatile_u32(&P.st->reverse)) {
-        U *a = (U *)P.a_keys;
-        const int64_t n = P.n, half = n / 2;
+        const int64_t r0 = (int64_t)P.st->run_split;
+        U *a = (U *)P.a_keys + r0;
+        uint32_t *av = KV ? P.a_vals + r0 : nullptr;
+        const int64_t n = P.n - r0, half = n / 2;
         const int64_t gt = (int64_t)blockIdx.x * THREADS + tid, gs = (int64_t)gridDim.x * THREADS;
         int64_t done = 0;
-        if (n % S::AL == 0) {
-            // 16-byte vectors from both ends (the array and its end are then 16-byte aligned): vector c of
+        if (n % S::AL == 0 && r0 % S::AL == 0) {
+            // 16-byte vectors from both ends (the range and its end are then 16-byte aligned): vector c of
             // the front swaps with vector c of the back, each reversed in registers
             constexpr int V = S::VEC;
             const int64_t nv = half / S::AL * S::AL / V;  // key vectors per side (whole payload vectors too)
@@ -2991,8 +3338,8 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
             if (KV) {
                 const int64_t nw = half / S::AL * S::AL / 4;
                 for (int64_t c = gt; c < nw; c += gs) {
-                    uint4 *f = reinterpret_cast<uint4 *>(P.a_vals + c * 4);
-                    uint4 *bk = reinterpret_cast<uint4 *>(P.a_vals + n - (c + 1) * 4);
+                    uint4 *f = reinterpret_cast<uint4 *>(av + c * 4);
+                    uint4 *bk = reinterpret_cast<uint4 *>(av + n - (c + 1) * 4);
                     const uint4 x = *f, y = *bk;
                     *f = make_uint4(y.w, y.z, y.y, y.x);
                     *bk = make_uint4(x.w, x.z, x.y, x.x);
@@ -3000,15 +3347,15 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
             }
             done = half / S::AL * S::AL;
         }
-        for (int64_t i = done + gt; i < half; i += gs) {  // the rest (or all of an unaligned length)
+        for (int64_t i = done + gt; i < half; i += gs) {  // the rest (or all of an unaligned range)
             const int64_t j = n - 1 - i;
             U x = a[i];
             a[i] = a[j];
             a[j] = x;
             if (KV) {
-                uint32_t y = P.a_vals[i];
-                P.a_vals[i] = P.a_vals[j];
-                P.a_vals[j] = y;
+                uint32_t y = av[i];
+                av[i] = av[j];
+                av[j] = y;
             }
         }
         __syncthreads();

@@ -48,7 +48,10 @@ class SortConfig:
     ``use_block_partition`` is a no-op (the partition is always branchless),
     ``use_partition_left`` gates the equal-key split (K3),
     ``use_break_patterns`` gates the sample perturbation after a bad
-    partition, and ``use_partial_insertion`` gates the sortedness check (K4).
+    partition, and ``use_partial_insertion`` gates the sortedness check (K4):
+    sorted input returns after one pass, reversed input after a reversal, and a
+    sorted prefix of at least half the array (``n >= two_run_min``) is merged
+    with the separately handled rest.
     """
 
     insertion_threshold: int = 24
@@ -63,6 +66,7 @@ class SortConfig:
     # ---- GPU fields ----
     base_case_size: int = 32768  # clamped to each element type's base-case capacity
     bad_budget: int = -1
+    two_run_min: int = 0  # smallest n for K4's two-run path (0: the library default, 2^18)
 
     def __post_init__(self):
         # driver.py:65-75, same messages
@@ -82,6 +86,8 @@ class SortConfig:
             raise ValueError("base_case_size must be in [1024, 32768]")
         if self.bad_budget < -1:
             raise ValueError("bad_budget must be -1 (log2 n) or >= 0")
+        if not 0 <= self.two_run_min < 2**31:
+            raise ValueError("two_run_min must be in [0, 2**31)")
 
     def to_c(self) -> _lib.PdqConfig:
         c = _lib.PdqConfig()
@@ -90,6 +96,7 @@ class SortConfig:
             setattr(c, f, int(getattr(self, f)))
         for f in ("use_block_partition", "use_partition_left", "use_break_patterns", "use_partial_insertion"):
             setattr(c, f, 1 if getattr(self, f) else 0)
+        c.reserved[1] = int(self.two_run_min)
         return c
 
 

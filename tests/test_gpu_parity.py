@@ -252,7 +252,102 @@ def test_sorted_and_reversed_are_one_pass():
     got, _, st = gpu_sort(asc)
     assert same_bytes(got, asc) and st["partition_right_calls"] == 0 and st["check_result"] == 2
     got, _, st = gpu_sort(asc[::-1].copy())
-    assert same_bytes(got, asc) and st["partition_right_calls"] == 0 and st["check_result"] == 1
+    assert same_bytes(got, asc) and st["partition_right_calls"] == 0 and st["check_result"] & 3 == 1
+
+
+def _two_runs(rng, n, s, kind, dtype):
+    """sorted prefix of s elements, then an ascending (1), descending (2) or random (3) rest"""
+    if np.dtype(dtype).kind == "f":
+        x = rng.standard_normal(n).astype(dtype)
+    else:
+        info = np.iinfo(dtype)
+        x = rng.integers(info.min, info.max, n, dtype=dtype, endpoint=True)
+    x[:s].sort()
+    if kind == 1:
+        x[s:].sort()
+    elif kind == 2:
+        x[s:] = np.sort(x[s:])[::-1]
+    return x
+
+
+@pytest.mark.parametrize("dtype", DTYPES + ["kv"], ids=lambda d: d if isinstance(d, str) else np.dtype(d).name)
+def test_two_run_path_vs_oracle(dtype):
+    # K4's two-run path (a sorted prefix of >= n/2 merged with the rest; the optimistic path of
+    # driver.py:244-250 / small_sorts.py:76-115 restated for the GPU): every second-run kind, splits at the
+    # eligibility boundary and near the end, sizes around the merge tile (8192) and the leaf sizes
+    rng = np.random.default_rng(11)
+    cfg = SortConfig(two_run_min=64)
+    kd = np.int64 if dtype == "kv" else dtype
+    for n in (64, 100, 4097, 8192, 8193, 24577, 70001, (1 << 18) + 5):
+        for s in sorted({(n + 1) // 2, (n + 1) // 2 + 1, int(0.75 * n), n - 2, n - 1}):
+            for kind in (1, 2, 3):
+                keys = _two_runs(rng, n, s, kind, kd)
+                vals = rng.permutation(n).astype(np.uint32) if dtype == "kv" else None
+                got, gv, st = gpu_sort(keys, vals, cfg)
+                want, wv = oracle_sort(keys, vals)
+                assert same_bytes(got, want), (n, s, kind)
+                if vals is not None:
+                    assert same_bytes(gv, wv), (n, s, kind)
+                # (a random rest may by chance extend the prefix or be monotone: only the path is asserted)
+                assert st["run_split"] >= s or st["check_result"] & 3 != 3, (n, s, kind, st)
+
+
+def test_two_run_path_duplicates_and_kinds():
+    rng = np.random.default_rng(12)
+    cfg = SortConfig(two_run_min=64)
+    n, s = 100000, 60000
+    keys = np.concatenate([np.sort(rng.integers(0, 50, s)), np.sort(rng.integers(0, 50, n - s))]).astype(np.int32)
+    got, _, st = gpu_sort(keys, None, cfg)
+    assert same_bytes(got, np.sort(keys)) and st["run_split"] == s and (st["check_result"] >> 4) == 1
+    assert st["partition_right_calls"] == 0 and st["base_cases"] == 0
+    # (key, payload) pairs with duplicate keys across the runs: each run sorted as pairs
+    k64 = keys.astype(np.int64)
+    vals = rng.integers(0, 5, n).astype(np.uint32)
+    for a, b in ((0, s), (s, n)):
+        o = np.lexsort((vals[a:b], k64[a:b]))
+        k64[a:b], vals[a:b] = k64[a:b][o], vals[a:b][o]
+    got, gv, st = gpu_sort(k64, vals, cfg)
+    want, wv = oracle_sort(k64, vals)
+    assert same_bytes(got, want) and same_bytes(gv, wv) and st["run_split"] == s
+    # descending rest: reversed in place, no partition; below two_run_min the path is off
+    keys = np.concatenate([np.arange(s), np.arange(n - s)[::-1]]).astype(np.int32)
+    got, _, st = gpu_sort(keys, None, cfg)
+    assert same_bytes(got, np.sort(keys)) and (st["check_result"] >> 4) == 2 and st["partition_right_calls"] == 0
+    got, _, st = gpu_sort(keys, None, SortConfig(two_run_min=n + 1))
+    assert same_bytes(got, np.sort(keys)) and st["run_split"] == 0 and st["partition_right_calls"] >= 1
+    # use_partial_insertion=False switches K4 off altogether (driver.py:63)
+    got, _, st = gpu_sort(keys, None, SortConfig(two_run_min=64, use_partial_insertion=False))
+    assert same_bytes(got, np.sort(keys)) and st["run_split"] == 0
+
+
+def test_two_run_patterns_beat_uniform():
+    # BASELINE C2: ascending + random tail and organ pipe at 2^24 take the two-run path (default
+    # threshold) and finish well below the time of a uniform sort of the same size
+    from paper_2106_05123_b200 import DeviceSorter
+
+    n = 1 << 24
+    cases = {"C2.asc_tail": workloads.c2("asc_tail", n), "C2.organ": workloads.c2("organ", n),
+             "uniform": workloads.c1(n)}
+    ms = {}
+    for name, keys in cases.items():
+        src = torch.from_numpy(keys).to(DEV)
+        x = src.clone()
+        ds = DeviceSorter(n, x.dtype, False)
+        best = 1e9
+        for _ in range(4):
+            x.copy_(src)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            ds.run(x)
+            b.record()
+            st = ds.finish()
+            best = min(best, a.elapsed_time(b))
+        assert bool((x[1:] >= x[:-1]).all().item())
+        if name != "uniform":
+            assert st["run_split"] >= n // 2, (name, st)
+        ms[name] = best
+    assert ms["C2.asc_tail"] < 0.7 * ms["uniform"] and ms["C2.organ"] < 0.7 * ms["uniform"], ms
 
 
 def test_extreme_values_and_zeros():
