@@ -106,24 +106,81 @@ class PdqStats(ctypes.Structure):
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
+
+# One translation unit per element type (pdq_inst.cu compiled eight times) so the instantiations of the
+# persistent sorter and the leaf kernels build in parallel; (object name, source, extra -D flags)
+_INST = [
+    ("i32", "launch_i32", "uint32_t", "false", "false"),
+    ("i32_kv", "launch_i32_kv", "uint32_t", "false", "true"),
+    ("f32", "launch_f32", "uint32_t", "true", "false"),
+    ("f32_kv", "launch_f32_kv", "uint32_t", "true", "true"),
+    ("i64", "launch_i64", "uint64_t", "false", "false"),
+    ("i64_kv", "launch_i64_kv", "uint64_t", "false", "true"),
+    ("f64", "launch_f64", "uint64_t", "true", "false"),
+    ("f64_kv", "launch_f64_kv", "uint64_t", "true", "true"),
+]
+BUILD_DIR = os.path.join(HERE, "_build")
+
+
+def translation_units(only_i32: bool = False):
+    """(object stem, source file, -D flags) of every translation unit of libpdq_b200.so."""
+    units = [("capi", "pdq_capi.cu", ["-DPDQ_ONLY_I32"] if only_i32 else []),
+             ("host", "pdq_host.cu", []),
+             ("bucket", "pdq_bucket_capi.cu", [])]
+    for stem, name, u, fl, kv in (_INST[:1] if only_i32 else _INST):
+        units.append((f"inst_{stem}", "pdq_inst.cu",
+                      [f"-DPDQ_INST_NAME={name}", f"-DPDQ_INST_U={u}", f"-DPDQ_INST_FLOAT={fl}", f"-DPDQ_INST_KV={kv}"]))
+    return units
+
 
 _lock = threading.Lock()
 _lib = None
 
 
-def build(verbose: bool = False) -> str:
-    """Compile csrc/ into libpdq_b200.so for sm_100a (nvcc cross-compiles without a GPU)."""
+def build(verbose: bool = False, out: str = None, extra_flags=(), only_i32: bool = False, jobs: int = 0) -> str:
+    """Compile csrc/ into libpdq_b200.so for sm_100a (nvcc cross-compiles without a GPU): the
+    translation units are compiled in parallel into _build/*.o (an object newer than every source and
+    header, built with the same flags, is reused) and linked into one shared library."""
+    from concurrent.futures import ThreadPoolExecutor
+
     nvcc = os.environ.get("NVCC", "nvcc")
     if not os.path.exists(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
         nvcc = "/usr/local/cuda/bin/nvcc"
-    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-o", LIB_PATH, os.path.join(CSRC, "pdq_capi.cu"),
-           os.path.join(CSRC, "pdq_host.cu")]
+    out = out or LIB_PATH
+    tag = "" if out == LIB_PATH else "_" + os.path.splitext(os.path.basename(out))[0]
+    os.makedirs(BUILD_DIR, exist_ok=True)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE)]
+    newest = max(os.path.getmtime(f) for f in deps)
+    flags = [*NVCC_FLAGS, *extra_flags] + (["-Xptxas=-v"] if verbose else [])
+
+    def compile_one(unit):
+        stem, src, defs = unit
+        obj = os.path.join(BUILD_DIR, f"{stem}{tag}.o")
+        cmd = [nvcc, *flags, *defs, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+        stamp = obj + ".cmd"
+        line = " ".join(cmd)
+        if (os.path.exists(obj) and os.path.getmtime(obj) >= newest and os.path.exists(stamp)
+                and open(stamp).read() == line):
+            return obj, ""
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src} ({stem}):\n{r.stdout}\n{r.stderr}")
+        with open(stamp, "w") as f:
+            f.write(line)
+        return obj, r.stdout + r.stderr
+
+    units = translation_units(only_i32)
+    with ThreadPoolExecutor(max_workers=jobs or min(len(units), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, units))
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.run(cmd, check=True)
-    return LIB_PATH
+        for (stem, _, _), (_, log) in zip(units, results):
+            if log:
+                print(f"== {stem}\n{log}")
+    subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out,
+                    *[obj for obj, _ in results]], check=True)
+    return out
 
 
 def lib() -> ctypes.CDLL:

@@ -11,14 +11,14 @@
 #include <nvtx3/nvToolsExt.h>  // header-only; ranges are no-ops unless a profiler is attached
 
 #include "../../include/pdq_b200.h"
-#include "pdq_bucket.cuh"
-#include "pdq_kernels.cuh"
+#include "pdq_device.cuh"
+#include "pdq_err.h"
 
 using namespace pdq;
 
 static thread_local char g_err[512];
 
-static int set_err(int code, const char *fmt, const char *detail = "") {
+int pdq::set_err(int code, const char *fmt, const char *detail) {
     snprintf(g_err, sizeof(g_err), fmt, detail);
     return code;
 }
@@ -60,14 +60,8 @@ extern "C" int pdq_config_validate(const pdq_config *c) {
 namespace {
 
 constexpr int MIN_BASE = 1024;
-#ifndef PDQ_CHUNK_MAX
-#define PDQ_CHUNK_MAX 32  // tiles per ring task at most
-#endif
 #ifndef PDQ_RUNS_MIN
 #define PDQ_RUNS_MIN (1 << 18)  // K4 takes the two-run path (sorted prefix of >= n/2 + merge) from this size
-#endif
-#ifndef PDQ_CHUNK_DIV
-#define PDQ_CHUNK_DIV 2  // the root level gets about this many tasks per CTA
 #endif
 
 struct Layout {
@@ -124,132 +118,6 @@ Layout layout(int dtype, int has_payload, int64_t n) {
     off += a256((size_t)L.rslot_cap * RDIG * 8);
     L.total = off;
     return L;
-}
-
-struct LaunchInfo {
-    int sms = 0;
-    int occ = 0;
-    int occ_base = 0;
-};
-
-// 4-byte keys without payload: leaves of up to BIG_BASE - 4 (24572) keys sorted by k_base_big; 8-byte
-// keys and key-value sorts: leaves of up to 8188 elements sorted by k_base_wide
-template <class U, bool KV>
-constexpr bool big_leaves() {
-    return sizeof(U) == 4 && !KV;
-}
-
-template <class U, bool FLOAT, bool KV>
-int smem_bytes() {
-    return Bufs<U, KV>::bytes();
-}
-
-constexpr int MAX_DEVS = 64;
-
-template <class U, bool FLOAT, bool KV>
-cudaError_t prepare(LaunchInfo &li) {
-    // per device and element type: kernel attributes set once, occupancy and SM count cached
-    static std::mutex mu;
-    static bool ready[MAX_DEVS] = {};
-    static LaunchInfo cache[MAX_DEVS];
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    if (dev < 0 || dev >= MAX_DEVS) return cudaErrorInvalidDevice;
-    std::lock_guard<std::mutex> g(mu);
-    LaunchInfo &cached = cache[dev];
-    if (!ready[dev]) {
-        const int sm = smem_bytes<U, FLOAT, KV>();
-        if ((e = cudaFuncSetAttribute(k_sort<U, FLOAT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) !=
-            cudaSuccess)
-            return e;
-        if ((e = cudaFuncSetAttribute(k_init<U, FLOAT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)) !=
-            cudaSuccess)
-            return e;
-        if constexpr (big_leaves<U, KV>()) {
-            if ((e = cudaFuncSetAttribute(k_base_big<FLOAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          BigLeaf<FLOAT>::bytes())) != cudaSuccess)
-                return e;
-            if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached.occ_base, k_base_big<FLOAT>, BigLeaf<FLOAT>::BT,
-                                                                   BigLeaf<FLOAT>::bytes())) != cudaSuccess)
-                return e;
-        } else {
-            if ((e = cudaFuncSetAttribute(k_base_wide<U, FLOAT, KV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          WideLeaf<U, FLOAT, KV>::bytes())) != cudaSuccess)
-                return e;
-            cached.occ_base = 1;
-        }
-        if (cached.occ_base < 1) cached.occ_base = 1;
-        if ((e = cudaDeviceGetAttribute(&cached.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached.occ, k_sort<U, FLOAT, KV>, THREADS, sm)) !=
-            cudaSuccess)
-            return e;
-        if (cached.occ < 1) cached.occ = 1;
-        ready[dev] = true;
-    }
-    li = cached;
-    return cudaSuccess;
-}
-
-// Programmatic dependent launch: the kernel may be scheduled while the previous kernel of the stream is
-// still running (its CTAs wait in griddepcontrol.wait until that kernel has completed and its memory is
-// visible), so the launch latency of each of the sort's kernels overlaps its predecessor's tail.
-template <class... KArgs, class... Args>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
-                       bool pdl, Args... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(block);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kernel, args...);
-}
-
-template <class U, bool FLOAT, bool KV>
-int launch(Params &P, cudaStream_t s, const Layout &L, cudaEvent_t ev0, cudaEvent_t ev1, cudaEvent_t ev_end) {
-    LaunchInfo li;
-    // (k_base_big reads a leaf as 16-byte vectors from its aligned base: up to 3 slots of lead-in)
-    const int base_max = big_leaves<U, KV>() ? BIG_BASE - 4 : WideLeaf<U, FLOAT, KV>::CAP - 4;
-    if (P.base_size > base_max) P.base_size = base_max;
-    cudaError_t e = prepare<U, FLOAT, KV>(li);
-    if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "setup: %s", cudaGetErrorString(e));
-    const int sm = smem_bytes<U, FLOAT, KV>();
-    {  // tiles per task: the largest power of two <= 32 giving the root ~2 tasks per CTA
-        constexpr int TL = Sorter<U, FLOAT, KV>::TL;
-        const int64_t per = ((P.n + TL - 1) / TL) / (PDQ_CHUNK_DIV * (int64_t)li.sms * li.occ);
-        uint32_t c = 1;
-        while (c < PDQ_CHUNK_MAX && (int64_t)(c * 2) <= per) c *= 2;
-        P.chunk = c;
-    }
-    if (P.use_check && P.n > 1) {
-        const int64_t ch = (int64_t)THREADS * ITEMS;
-        int64_t blocks = (P.n + ch - 1) / ch;
-        const int64_t cap = (int64_t)li.sms * 8;
-        if (blocks > cap) blocks = cap;
-        k_check<U, FLOAT, KV><<<(unsigned)blocks, THREADS, 0, s>>>(P);
-    }
-    // (an event between two kernels ends the programmatic overlap there: timed runs measure each kernel)
-    e = launch_pdl(k_init<U, FLOAT, KV>, 1, THREADS, sm, s, P.use_check && P.n > 1, P);
-    if (e == cudaSuccess && ev0) cudaEventRecord(ev0, s);
-    if (e == cudaSuccess) e = launch_pdl(k_sort<U, FLOAT, KV>, (unsigned)(li.sms * li.occ), THREADS, sm, s, !ev0, P);
-    if (e == cudaSuccess && ev1) cudaEventRecord(ev1, s);
-    if (e == cudaSuccess) {
-        if constexpr (big_leaves<U, KV>())
-            e = launch_pdl(k_base_big<FLOAT>, (unsigned)(li.sms * li.occ_base), BigLeaf<FLOAT>::BT,
-                           BigLeaf<FLOAT>::bytes(), s, !ev1, P);
-        else
-            e = launch_pdl(k_base_wide<U, FLOAT, KV>, (unsigned)li.sms, 1024, WideLeaf<U, FLOAT, KV>::bytes(), s, !ev1,
-                           P);
-    }
-    if (e == cudaSuccess && ev_end) cudaEventRecord(ev_end, s);
-    if (e == cudaSuccess) e = cudaGetLastError();
-    if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "launch: %s", cudaGetErrorString(e));
-    return PDQ_OK;
 }
 
 }  // namespace
@@ -336,14 +204,14 @@ extern "C" int pdq_sort_timed(void *keys, int dtype, uint32_t *payload, int64_t 
 
     const bool kv = payload != nullptr;
 #ifdef PDQ_ONLY_I32  // profiling builds (tools/): int32 keys-only instantiation, fast to compile
-    if (dtype == PDQ_I32 && !kv) return launch<uint32_t, false, false>(P, s, L, ev0, ev1, eve);
+    if (dtype == PDQ_I32 && !kv) return launch_i32(P, s, ev0, ev1, eve);
     return set_err(PDQ_ERR_DTYPE, "this profiling build sorts int32 keys only%s");
 #else
     switch (dtype) {
-        case PDQ_I32: return kv ? launch<uint32_t, false, true>(P, s, L, ev0, ev1, eve) : launch<uint32_t, false, false>(P, s, L, ev0, ev1, eve);
-        case PDQ_F32: return kv ? launch<uint32_t, true, true>(P, s, L, ev0, ev1, eve) : launch<uint32_t, true, false>(P, s, L, ev0, ev1, eve);
-        case PDQ_I64: return kv ? launch<uint64_t, false, true>(P, s, L, ev0, ev1, eve) : launch<uint64_t, false, false>(P, s, L, ev0, ev1, eve);
-        case PDQ_F64: return kv ? launch<uint64_t, true, true>(P, s, L, ev0, ev1, eve) : launch<uint64_t, true, false>(P, s, L, ev0, ev1, eve);
+        case PDQ_I32: return kv ? launch_i32_kv(P, s, ev0, ev1, eve) : launch_i32(P, s, ev0, ev1, eve);
+        case PDQ_F32: return kv ? launch_f32_kv(P, s, ev0, ev1, eve) : launch_f32(P, s, ev0, ev1, eve);
+        case PDQ_I64: return kv ? launch_i64_kv(P, s, ev0, ev1, eve) : launch_i64(P, s, ev0, ev1, eve);
+        case PDQ_F64: return kv ? launch_f64_kv(P, s, ev0, ev1, eve) : launch_f64(P, s, ev0, ev1, eve);
     }
 #endif
     return set_err(PDQ_ERR_DTYPE, "unsupported dtype code%s");
@@ -388,104 +256,3 @@ extern "C" int pdq_sort_finish(void *workspace, pdq_stats *out, void *stream) {
     return PDQ_OK;
 }
 
-// ---- sample-sort bucketing ----------------------------------------
-
-extern "C" size_t pdq_bucket_workspace_bytes(int64_t n, int nbuckets) {
-    if (n < 0 || nbuckets < 1 || nbuckets > BK_MAX) return 0;
-    return a256((size_t)nbuckets * (size_t)BK_MAX_CTAS * sizeof(int64_t));  // any element type's grid
-}
-
-__global__ void k_set_i64(int64_t *p, int64_t v) { *p = v; }
-
-namespace {
-template <class U, bool FLOAT, bool KV, int LT>
-int launch_bucket(const void *keys, const uint32_t *vals, int64_t n, int64_t gidx_base, const void *sk,
-                  const uint32_t *sv, const int64_t *sg, int ns, void *ok, uint32_t *ov, int64_t *bucket_counts,
-                  int64_t *cnt, cudaStream_t s) {
-    const BucketGeom g = bucket_geom(n, BkShape<U, KV>::TILE, BkShape<U, KV>::CTAS);
-    const int nb = ns + 1;
-    const size_t hist = (size_t)nb * BK_THREADS * sizeof(uint32_t);
-    const size_t sc = sizeof(ScatterSmem<U, KV>) + hist;
-    cudaError_t ea = cudaFuncSetAttribute(k_bucket_count<U, FLOAT, KV, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)(BK_MAX * BK_THREADS * sizeof(uint32_t)));
-    if (ea == cudaSuccess)
-        ea = cudaFuncSetAttribute(k_bucket_scatter<U, FLOAT, KV, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(ScatterSmem<U, KV>) + BK_MAX * BK_THREADS * sizeof(uint32_t)));
-    if (ea != cudaSuccess) return set_err(PDQ_ERR_CUDA, "bucket setup: %s", cudaGetErrorString(ea));
-    k_bucket_count<U, FLOAT, KV, LT><<<g.ctas, BK_THREADS, hist, s>>>((const U *)keys, vals, n, gidx_base,
-                                                                         (const U *)sk, sv, sg, ns, cnt, g);
-    k_bucket_scan<<<1, BK_SCAN_THREADS, 0, s>>>(cnt, (int64_t)nb * g.ctas, nb, g.ctas, bucket_counts);
-    k_bucket_scatter<U, FLOAT, KV, LT><<<g.ctas, BK_THREADS, sc, s>>>(
-        (const U *)keys, vals, n, gidx_base, (const U *)sk, sv, sg, ns, cnt, (U *)ok, ov, g);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return set_err(PDQ_ERR_CUDA, "bucket launch: %s", cudaGetErrorString(e));
-    return PDQ_OK;
-}
-
-template <class U, bool FLOAT, bool KV>
-int launch_bucket_nb(const void *keys, const uint32_t *vals, int64_t n, int64_t gidx_base, const void *sk,
-                     const uint32_t *sv, const int64_t *sg, int ns, void *ok, uint32_t *ov, int64_t *bucket_counts,
-                     int64_t *cnt, cudaStream_t s) {
-    // up to 8 buckets (one NVLink node): per-thread counts packed in registers, the splitter search
-    // unrolled to its depth
-#define PDQ_LB(LT) launch_bucket<U, FLOAT, KV, LT>(keys, vals, n, gidx_base, sk, sv, sg, ns, ok, ov, bucket_counts, cnt, s)
-    switch (bucket_log2(ns + 1)) {
-        case 0: return PDQ_LB(0);
-        case 1: return PDQ_LB(1);
-        case 2: return PDQ_LB(2);
-        case 3: return PDQ_LB(3);
-        default: return PDQ_LB(-1);
-    }
-#undef PDQ_LB
-}
-}  // namespace
-
-extern "C" int pdq_bucket(const void *keys, int dtype, const uint32_t *payload, int64_t n, int64_t gidx_base,
-                          const void *split_keys, const uint32_t *split_payload, const int64_t *split_gidx,
-                          int nsplit, void *out_keys, uint32_t *out_payload, int64_t *bucket_counts,
-                          void *workspace, size_t ws_bytes, void *stream) {
-    if (dtype_size(dtype) == 0) return set_err(PDQ_ERR_DTYPE, "unsupported dtype code%s");
-    if (n < 0) return set_err(PDQ_ERR_ARG, "n must be >= 0%s");
-    if (nsplit < 0 || nsplit + 1 > BK_MAX) return set_err(PDQ_ERR_ARG, "nsplit must be in [0, 63]%s");
-    if (!bucket_counts) return set_err(PDQ_ERR_ARG, "bucket_counts is NULL%s");
-    if (n > 0 && (!keys || !out_keys)) return set_err(PDQ_ERR_ARG, "keys / out_keys is NULL%s");
-    if ((payload == nullptr) != (out_payload == nullptr))
-        return set_err(PDQ_ERR_ARG, "payload and out_payload must both be given or both be NULL%s");
-    if (nsplit > 0 && (!split_keys || !split_gidx || (payload && !split_payload)))
-        return set_err(PDQ_ERR_ARG, "splitter arrays are NULL%s");
-    const size_t need = pdq_bucket_workspace_bytes(n, nsplit + 1);
-    if (!workspace || ws_bytes < need) return set_err(PDQ_ERR_WORKSPACE, "bucket workspace too small%s");
-    cudaStream_t s = (cudaStream_t)stream;
-    if (n == 0) {
-        cudaError_t e = cudaMemsetAsync(bucket_counts, 0, (size_t)(nsplit + 1) * sizeof(int64_t), s);
-        return e == cudaSuccess ? PDQ_OK : set_err(PDQ_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
-    }
-    if (((uintptr_t)keys & 15) || ((uintptr_t)payload & 15))
-        return set_err(PDQ_ERR_ALIGN, "keys and payload must be 16-byte aligned%s");
-    if (nsplit == 0) {  // one bucket: a copy
-        const int64_t cn = n;
-        cudaError_t e = cudaMemcpyAsync(out_keys, keys, (size_t)n * dtype_size(dtype), cudaMemcpyDeviceToDevice, s);
-        if (e == cudaSuccess && payload)
-            e = cudaMemcpyAsync(out_payload, payload, (size_t)n * 4, cudaMemcpyDeviceToDevice, s);
-        if (e == cudaSuccess) {  // the one bucket's size, written by the device (no host staging)
-            k_set_i64<<<1, 1, 0, s>>>(bucket_counts, cn);
-            e = cudaGetLastError();
-        }
-        return e == cudaSuccess ? PDQ_OK : set_err(PDQ_ERR_CUDA, "bucket copy: %s", cudaGetErrorString(e));
-    }
-    int64_t *cnt = (int64_t *)workspace;
-    const bool kv = payload != nullptr;
-#define PDQ_BK(U, F) \
-    (kv ? launch_bucket_nb<U, F, true>(keys, payload, n, gidx_base, split_keys, split_payload, split_gidx, nsplit, \
-                                    out_keys, out_payload, bucket_counts, cnt, s)                              \
-        : launch_bucket_nb<U, F, false>(keys, payload, n, gidx_base, split_keys, split_payload, split_gidx, nsplit, \
-                                     out_keys, out_payload, bucket_counts, cnt, s))
-    switch (dtype) {
-        case PDQ_I32: return PDQ_BK(uint32_t, false);
-        case PDQ_F32: return PDQ_BK(uint32_t, true);
-        case PDQ_I64: return PDQ_BK(uint64_t, false);
-        case PDQ_F64: return PDQ_BK(uint64_t, true);
-    }
-#undef PDQ_BK
-    return set_err(PDQ_ERR_DTYPE, "unsupported dtype code%s");
-}

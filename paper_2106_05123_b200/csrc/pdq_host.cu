@@ -66,7 +66,7 @@ void copy_nt(unsigned char *dst, const unsigned char *src, size_t n) {
     memcpy(dst, src, n);
 }
 
-constexpr size_t CHUNK_DEFAULT = 2u << 20;  // bytes per staging slot ($PDQ_HOST_CHUNK_KB overrides)
+constexpr size_t CHUNK_DEFAULT = 4u << 20;  // bytes per staging slot ($PDQ_HOST_CHUNK_KB overrides; tools/host_sweep.py)
 constexpr int MAX_SLOTS = 8;               // staging slots per worker ($PDQ_HOST_SLOTS, default 2)
 
 struct Seg1 {  // one array to transfer: host <-> device, `bytes` long
@@ -152,10 +152,36 @@ struct ChunkRef {
     const Seg1 *s;
     size_t off, bytes;
 };
-std::vector<ChunkRef> chunk_list(const std::vector<Seg1> &segs, size_t chunk) {
+// Chunks of `chunk` bytes, except that the first and the last `workers` chunks of the whole transfer
+// ramp up from / taper down to chunk / 8 (three rounds each): the first DMA starts after a short host
+// copy instead of a full slot, and the last host copy-out after the final DMA is short
+// ($PDQ_HOST_RAMP=0: equal chunks).
+bool g_ramp = true;
+std::vector<ChunkRef> chunk_list(const std::vector<Seg1> &segs, size_t chunk, int workers) {
     std::vector<ChunkRef> out;
-    for (const Seg1 &s : segs)
-        for (size_t off = 0; off < s.bytes; off += chunk) out.push_back({&s, off, std::min(chunk, s.bytes - off)});
+    size_t total = 0;
+    for (const Seg1 &s : segs) total += s.bytes;
+    const size_t gran = 64u << 10;
+    const bool ramp = g_ramp && chunk >= 8 * gran && total >= (size_t)workers * chunk * 8;
+    size_t done = 0;  // bytes of the whole transfer before the current position
+    const size_t edge = ramp ? (size_t)workers * (chunk / 8 + chunk / 4 + chunk / 2) : 0;
+    auto size_at = [&](size_t pos) -> size_t {  // size of the chunk that starts `pos` bytes into the transfer
+        if (!ramp) return chunk;
+        const size_t w = (size_t)workers;
+        const size_t d = std::min(pos, total - pos - 1);  // distance from the nearer end (the tail mirrors the head)
+        if (d < w * (chunk / 8)) return chunk / 8;
+        if (d < w * (chunk / 8 + chunk / 4)) return chunk / 4;
+        if (d < edge) return chunk / 2;
+        return chunk;
+    };
+    for (const Seg1 &s : segs) {
+        for (size_t off = 0; off < s.bytes;) {
+            const size_t c = std::min(size_at(done + off), s.bytes - off);
+            out.push_back({&s, off, c});
+            off += c;
+        }
+        done += s.bytes;
+    }
     return out;
 }
 
@@ -238,6 +264,7 @@ extern "C" pdq_host_sorter *pdq_host_sorter_create(int device, int threads) {
     }
     h->nthreads = std::min(threads, 64);
     if (const char *nt = getenv("PDQ_HOST_NT")) g_nt = atoi(nt) != 0;
+    if (const char *rp = getenv("PDQ_HOST_RAMP")) g_ramp = atoi(rp) != 0;
     if (const char *sl = getenv("PDQ_HOST_SLOTS")) h->nslots = std::max(2, std::min(MAX_SLOTS, atoi(sl)));
     if (const char *ck = getenv("PDQ_HOST_CHUNK_KB")) {
         const long kb = atol(ck);
@@ -318,7 +345,7 @@ extern "C" int pdq_host_sort(pdq_host_sorter *h, void *keys, int dtype, uint32_t
     // chunks: the slot size, or smaller so that a small array still spreads over every worker
     size_t ck = (kb + vb + h->nthreads - 1) / h->nthreads;
     ck = std::max<size_t>(64u << 10, std::min(h->chunk, (ck + (64u << 10) - 1) & ~(size_t)((64u << 10) - 1)));
-    const std::vector<ChunkRef> ch = chunk_list(segs, ck);
+    const std::vector<ChunkRef> ch = chunk_list(segs, ck, h->nthreads);
     for (Worker &wk : h->w) wk.rc = 0;
 
     // 1. H2D through the pinned slots (all workers)
