@@ -3106,6 +3106,7 @@ struct RunsMerge {
         }
         bsync();
         const int64_t o0 = bd[0], r2e = bd[1];
+        PDQ_CHECK(o0 >= 0 && o0 <= s && r2e >= s && r2e <= n && (o0 & 7) == 0, "merge window");
         const int64_t len1 = s - o0, len2 = r2e - s, m = len1 + len2;
         bsync();
         const int64_t ntiles = (m + T - 1) / T;
@@ -3133,8 +3134,10 @@ struct RunsMerge {
                 const int L1 = (int)(bd[k + 1] - i0), L = (int)(d1 - d0);
                 U *kd = kin((int)(k & 1));
                 uint32_t *vd = vin((int)(k & 1));
+                PDQ_CHECK(L1 >= 0 && L1 <= L && L <= T && j0 >= 0, "merge tile boundaries are monotone");
                 for (int x = tid; x < L; x += BT) {
                     const int64_t src = x < L1 ? o0 + i0 + x : s + j0 + (x - L1);
+                    PDQ_CHECK(src >= 0 && src < P.n && (x < L1 ? src < s : src >= s), "merge tile source inside its run");
                     cp_async(kd + x, a + src);
                     if constexpr (KV) cp_async(vd + x, P.a_vals + src);
                 }
@@ -3185,6 +3188,7 @@ struct RunsMerge {
                     }
                 }
                 U *dst = b + o0 + d0 + dl;
+                PDQ_CHECK(o0 + d0 + L <= P.n, "merge tile output inside the array");
                 if (dl + V <= L) {  // o0 + d0 + dl is a multiple of 8 elements: 16-byte aligned vectors
                     constexpr int KPV = 16 / (int)sizeof(U);
 #pragma unroll

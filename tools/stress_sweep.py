@@ -1,5 +1,5 @@
 """Stress sweep (run it with a PDQ_DEBUG build: device-side bounds asserts): every dtype, KV, the
-leaf slow paths, K3 (low cardinality), K4 (sorted / reversed), the K5 radix fallback.
+leaf slow paths, K3 (low cardinality), K4 (sorted / reversed / two runs), the K5 radix fallback.
 
   tools/build_debug.sh && PDQ_LIB=tools/libdebug.so python tools/stress_sweep.py
 (compute-sanitizer is not available on the GPU pool.)
@@ -43,4 +43,18 @@ for n in (0, 1, 5, 64, 65, 4097, 16385, 70001, 300000):
 check(rng.integers(-2**31, 2**31, 300000).astype(np.int32), cfg=SortConfig(bad_budget=0))
 check(rng.integers(-2**31, 2**31, 300000).astype(np.int64), rng.integers(0, 2**32, 300000, dtype=np.uint32),
       cfg=SortConfig(bad_budget=0))
+# K4 two-run path: sorted prefix + ascending / descending / random rest, every dtype and KV
+cfg2 = SortConfig(two_run_min=64)
+for n in (64, 4097, 8193, 70001, 300000):
+    for dt in (np.int32, np.int64, np.float32, np.float64):
+        for kind in (1, 2, 3):
+            k = rng.integers(-2**31, 2**31, n).astype(dt) if dt in (np.int32, np.int64) else rng.standard_normal(n).astype(dt)
+            s = int(n * 0.6)
+            k[:s].sort()
+            if kind == 1:
+                k[s:].sort()
+            elif kind == 2:
+                k[s:] = np.sort(k[s:])[::-1]
+            check(k, cfg=cfg2)
+            check(k.astype(np.int64) if dt == np.int32 else k, rng.permutation(n).astype(np.uint32), cfg=cfg2)
 print("stress sweep ok")
