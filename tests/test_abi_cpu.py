@@ -49,6 +49,11 @@ def test_config_struct_layout_and_defaults():
     mine = DEFAULT_CONFIG.to_c()
     assert bytes(mine) == bytes(c)
     assert L.pdq_config_validate(ctypes.byref(c)) == 0
+    # GPU fields: two_run_min travels in reserved[1] (0 = the library default); out-of-range values raise
+    assert SortConfig(two_run_min=64).to_c().reserved[1] == 64 and mine.reserved[1] == 0
+    for bad in (-1, 2**31):
+        with pytest.raises(ValueError):
+            SortConfig(two_run_min=bad)
 
 
 @pytest.mark.parametrize("kw", [

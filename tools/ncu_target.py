@@ -16,7 +16,15 @@ g.manual_seed(1)
 src = torch.randint(-(2**31), 2**31, (n,), device="cuda", generator=g, dtype=torch.int64).to(torch.int32)
 which = sys.argv[1:] or ["normal", "fallback", "c5"]
 for w in which:
-    if w in ("normal", "fallback"):
+    if w == "organ":  # K4 two-run path: 2^24 organ pipe (k_check full pass, reversal, merge epilogue of k_base_big)
+        from paper_2106_05123_b200 import workloads
+        m = 1 << 24
+        x = torch.from_numpy(workloads.c2("organ", m)).cuda()
+        ds = DeviceSorter(m, torch.int32, False)
+        ds.run(x)
+        st = ds.finish()
+        print(w, bool((x[1:] >= x[:-1]).all().item()), st["run_split"], flush=True)
+    elif w in ("normal", "fallback"):
         ds = DeviceSorter(n, torch.int32, False, config=SortConfig(bad_budget=0 if w == "fallback" else -1))
         x = src.clone()
         ds.run(x)
