@@ -3018,20 +3018,22 @@ struct WideLeaf {
 };
 
 // ---- K4 two-run epilogue: merge A[0, s) and A[s, n) (both ascending) -----------------------------------
-// Runs in the leaf kernel's persistent CTAs (one 1024-thread CTA per SM, all resident) after the leaves:
-// grid barrier, merge-path tiles A -> B, grid barrier, copy B -> A.  A tile is T = 8192 outputs: its two
-// input ranges come from a merge-path search over global memory (every thread of a CTA searches one of
-// the CTA's tile boundaries, all at once), land in shared memory as ordered images, and every thread
-// merges V = 8 consecutive outputs from its own diagonal and stores them as 16-byte vectors.  Ties take
-// the first run's element (for keys-only sorts equal keys are identical bits; with a payload the order
-// is the (key, payload) order, so there are no ties between distinct elements).
+// Runs in the leaf kernel's persistent CTAs (one 1024-thread CTA per SM) after the leaves: wait until every
+// leaf is in A, merge-path tiles A -> B, wait until every tile is written, copy B -> A.  The waits are
+// progress counters, not grid barriers: leaves and tiles are claimed dynamically, so a CTA only waits for
+// work that a running CTA holds, and concurrent sorts that cannot be co-resident do not deadlock.  A tile
+// is T = 8192 outputs: its two input ranges come from a merge-path search over global memory (one warp per
+// tile boundary, 32 probes per round), land in shared memory by cp.async (double-buffered), and every
+// thread merges V = 8 consecutive outputs from its own diagonal and stores them as 16-byte vectors.  Ties
+// take the first run's element (for keys-only sorts equal keys are identical bits; with a payload the
+// order is the (key, payload) order, so there are no ties between distinct elements).
 template <class U, bool FLOAT, bool KV>
 struct RunsMerge {
     using O = Ord<U, FLOAT>;
-    static constexpr int BT = 1024, V = 8, T = BT * V, BATCH = 1024;
+    static constexpr int BT = 1024, V = 8, T = BT * V, BATCH = 32;
     // two stages of raw keys (+ payloads): tile k + 1 arrives by cp.async while tile k is merged
     static constexpr int VIN = T * (int)sizeof(U), STAGE = VIN + (KV ? T * 4 : 0), BND = 2 * STAGE;
-    __host__ __device__ static constexpr int bytes() { return BND + (BATCH + 1) * 8; }
+    __host__ __device__ static constexpr int bytes() { return BND + (BATCH + 2) * 8; }
     __device__ __forceinline__ static U *kin(int st) { return reinterpret_cast<U *>(g_dsm + st * STAGE); }
     __device__ __forceinline__ static uint32_t *vin(int st) {
         return reinterpret_cast<uint32_t *>(g_dsm + st * STAGE + VIN);
@@ -3044,13 +3046,11 @@ struct RunsMerge {
     }
     __device__ __forceinline__ static void bsync() { asm volatile("bar.sync 1, %0;" ::"n"(BT) : "memory"); }
 
-    __device__ static void grid_barrier(const Params &P, unsigned &round) {
+    // thread 0 waits until *counter >= target (bracketed by CTA barriers and gpu-scope fences)
+    __device__ static void wait_for(const unsigned long long *counter, unsigned long long target) {
         bsync();
         if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(&P.st->gbar, 1u);
-            const unsigned target = (++round) * gridDim.x;
-            while (ld_volatile_u32(&P.st->gbar) < target) __nanosleep(128);
+            while (*(const volatile unsigned long long *)counter < target) __nanosleep(128);
             __threadfence();
         }
         bsync();
@@ -3088,8 +3088,14 @@ struct RunsMerge {
         const U *a = (const U *)P.a_keys;
         U *b = (U *)P.b_keys;
         int64_t *bd = bnd();
-        unsigned round = 0;
-        grid_barrier(P, round);  // every leaf is in A
+        {  // every leaf is in A: this CTA's leaves are counted, then all of them awaited
+            unsigned long long total = *(volatile unsigned long long *)&P.st->leaf_count;
+            if (total > P.leaf_cap) total = P.leaf_cap;
+            __threadfence();
+            bsync();
+            if (tid == 0 && sh.s_base) atomicAdd(&P.st->leaves_done, sh.s_base);
+            wait_for(&P.st->leaves_done, total);
+        }
         // The window that changes: first-run elements <= the second run's smallest stay where they are, and
         // so do second-run elements >= the first run's largest (appending slightly newer keys to a sorted
         // array merges only the overlap).  The window starts at a multiple of 8 elements (16-byte stores).
@@ -3110,12 +3116,18 @@ struct RunsMerge {
         const int64_t len1 = s - o0, len2 = r2e - s, m = len1 + len2;
         bsync();
         const int64_t ntiles = (m + T - 1) / T;
-        const int64_t per = (ntiles + gridDim.x - 1) / gridDim.x;  // consecutive tiles of this CTA
-        const int64_t t_lo = (int64_t)blockIdx.x * per, t_hi = t_lo + per < ntiles ? t_lo + per : ntiles;
+        // tiles are claimed in batches of consecutive tiles: one batch per CTA when every CTA is running (each
+        // batch pays one round of boundary searches), at most 32 tiles (one warp per boundary)
+        int64_t batch = (ntiles + gridDim.x - 1) / gridDim.x;
+        batch = batch < 1 ? 1 : (batch > BATCH ? BATCH : batch);
         unsigned long long moved = 0;
-        for (int64_t tb = t_lo; tb < t_hi; tb += BATCH) {
-            const int64_t nb = t_hi - tb < BATCH ? t_hi - tb : BATCH;
+        for (;;) {
             bsync();
+            if (tid == 0) bd[BATCH + 1] = (int64_t)atomicAdd(&P.st->merge_next, (unsigned long long)batch);
+            bsync();
+            const int64_t tb = bd[BATCH + 1];
+            if (tb >= ntiles) break;
+            const int64_t nb = ntiles - tb < batch ? ntiles - tb : batch;
             // merge path: first-run elements among the first d outputs, one boundary per warp at a time
             for (int64_t k = warp; k <= nb; k += BT / 32) {
                 const int64_t d = (tb + k) * T < m ? (tb + k) * T : m;
@@ -3217,8 +3229,11 @@ struct RunsMerge {
                 moved += (tid == 0) ? (unsigned long long)L : 0ull;
                 bsync();
             }
+            __threadfence();  // this batch's tiles are in B
+            bsync();
+            if (tid == 0) atomicAdd(&P.st->merge_done, (unsigned long long)nb);
         }
-        grid_barrier(P, round);  // B holds the merged array
+        wait_for(&P.st->merge_done, (unsigned long long)ntiles);  // B holds the merged window
         {  // copy the window back, 16-byte vectors (o0 is a multiple of 8 elements)
             constexpr int KPV = 16 / (int)sizeof(U);
             const int64_t gt = (int64_t)blockIdx.x * BT + tid, gs = (int64_t)gridDim.x * BT;
@@ -3351,15 +3366,34 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
             }
             done = half / S::AL * S::AL;
         }
-        for (int64_t i = done + gt; i < half; i += gs) {  // the rest (or all of an unaligned range)
-            const int64_t j = n - 1 - i;
-            U x = a[i];
-            a[i] = a[j];
-            a[j] = x;
-            if (KV) {
-                uint32_t y = av[i];
-                av[i] = av[j];
-                av[j] = y;
+        // the rest (or all of an unaligned range: the second of two runs starts anywhere): element swaps,
+        // four independent pairs in flight per thread
+        for (int64_t i0 = done + gt; i0 < half; i0 += 4 * gs) {
+            U x[4], y[4];
+            uint32_t xv[4], yv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t i = i0 + q * gs;
+                if (i < half) {
+                    x[q] = a[i];
+                    y[q] = a[n - 1 - i];
+                    if (KV) {
+                        xv[q] = av[i];
+                        yv[q] = av[n - 1 - i];
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t i = i0 + q * gs;
+                if (i < half) {
+                    a[i] = y[q];
+                    a[n - 1 - i] = x[q];
+                    if (KV) {
+                        av[i] = yv[q];
+                        av[n - 1 - i] = xv[q];
+                    }
+                }
             }
         }
         __syncthreads();

@@ -429,6 +429,34 @@ def test_concurrent_streams_distinct_workspaces():
         assert np.array_equal(d.cpu().numpy(), np.sort(a))
 
 
+def test_concurrent_two_run_sorts_do_not_deadlock():
+    # the merge epilogue of the leaf kernel waits on progress counters, not grid barriers: four sorts that
+    # all take the two-run path on different streams (their one-CTA-per-SM leaf kernels cannot be
+    # co-resident) must all finish
+    from paper_2106_05123_b200 import DeviceSorter
+
+    rng = np.random.default_rng(10)
+    n = 1 << 22
+    arrs = []
+    for kind in (1, 2, 3, 3):
+        arrs.append(_two_runs(rng, n, int(0.7 * n), kind, np.int32))
+    streams = [torch.cuda.Stream() for _ in arrs]
+    devs = [torch.from_numpy(a).to(DEV) for a in arrs]
+    sorters = [DeviceSorter(n, torch.int32, False) for _ in arrs]
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for d, a in zip(devs, arrs):
+            d.copy_(torch.from_numpy(a))
+        torch.cuda.synchronize()
+        for d, ds, s in zip(devs, sorters, streams):
+            with torch.cuda.stream(s):
+                ds.run(d)
+        for a, d, ds, s in zip(arrs, devs, sorters, streams):
+            st = ds.finish(s)
+            assert st["run_split"] > 0
+            assert np.array_equal(d.cpu().numpy(), np.sort(a))
+
+
 def test_repeated_sorts_reuse_workspace():
     from paper_2106_05123_b200 import DeviceSorter
 
