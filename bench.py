@@ -452,8 +452,10 @@ def run_ours(args, rank, world, local_rank):
         # (device counter, SURVEY.md §8(d) byte model over the segments it processed) / its event time
         bytes_launch = kstats["bytes_algorithmic"]  # the kernel-timing pass's sorts (same inputs)
         leaf_kernel = "k_base_big" if (not kv and k0.itemsize == 4) else "k_base_wide"
-        traffic, traffic_src = ncu_traffic("k_sort")
-        ltraffic, _ = ncu_traffic(leaf_kernel)
+        # ncu DRAM bytes per launch: the committed captures are of the R workload (k_sort, k_base_big) and of
+        # the C5 recipe (k_base_wide); other configs report no traffic figure
+        traffic, traffic_src = ncu_traffic("k_sort") if cfg == "R" else (None, None)
+        ltraffic, _ = ncu_traffic(leaf_kernel) if cfg in ("R", "C5") else (None, None)
         ks_ms = statistics.mean(ksort_ms)
         lf_ms = statistics.mean(leaf_ms)
         achieved = bytes_launch / (ks_ms / 1e3) / 1e9
