@@ -68,7 +68,7 @@ typedef struct pdq_config {
                                          radix fallback on the first big segment: test knob) */
     int32_t reserved[4];              /* reserved[0] > 0: profiling knob, stop descending at that
                                          depth (output NOT sorted); keep 0.
-                                         reserved[1] > 0: smallest n for K4's two-run path (default 2^18;
+                                         reserved[1] > 0: smallest n for K4's two-run path (default 2^15;
                                          tests lower it) */
 } pdq_config;
 

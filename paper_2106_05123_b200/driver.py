@@ -66,7 +66,7 @@ class SortConfig:
     # ---- GPU fields ----
     base_case_size: int = 32768  # clamped to each element type's base-case capacity
     bad_budget: int = -1
-    two_run_min: int = 0  # smallest n for K4's two-run path (0: the library default, 2^18)
+    two_run_min: int = 0  # smallest n for K4's two-run path (0: the library default, 2^15)
 
     def __post_init__(self):
         # driver.py:65-75, same messages

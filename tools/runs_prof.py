@@ -1,23 +1,27 @@
-"""Per-kernel spans of the K4 two-run path on the C2 patterns (device timers): python tools/runs_prof.py [log2n]"""
+"""Per-kernel spans of the K4 two-run path on the C2 patterns (device timers):
+  python tools/runs_prof.py [log2n] [two_run_min]"""
 import sys
 
 import numpy as np
 import torch
 
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
-from paper_2106_05123_b200 import DeviceSorter, workloads  # noqa: E402
+from paper_2106_05123_b200 import DeviceSorter, SortConfig, workloads  # noqa: E402
 
 lg = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+cfg = SortConfig(two_run_min=int(sys.argv[2])) if len(sys.argv) > 2 else SortConfig()
 n = 1 << lg
 rng = np.random.default_rng(3)
 app = np.arange(n, dtype=np.int32)
 app[n - n // 100:] = np.sort(rng.integers(n - n // 50, n, n // 100)).astype(np.int32)  # newer keys, overlapping 2 %
-cases = {"asc": workloads.c2("asc", n), "organ": workloads.c2("organ", n), "asc_tail": workloads.c2("asc_tail", n),
+half = workloads.c1(n).copy()
+half[: n // 2].sort()
+cases = {"sort50": half, "asc": workloads.c2("asc", n), "organ": workloads.c2("organ", n), "asc_tail": workloads.c2("asc_tail", n),
          "append_overlap": app, "uniform": workloads.c1(n)}
 for name, keys in cases.items():
     src = torch.from_numpy(keys).cuda()
     x = src.clone()
-    ds = DeviceSorter(n, x.dtype, False)
+    ds = DeviceSorter(n, x.dtype, False, config=cfg)
     rows = []
     for r in range(6):
         x.copy_(src)
