@@ -84,9 +84,10 @@ typedef struct pdq_stats {
     int64_t bytes_algorithmic;      /* SURVEY.md §8(d) byte model over the init + sorter kernels, summed
                                        over the segments they actually processed */
     int64_t check_result;           /* K4: bit0 a descent seen, bit1 an ascent seen, bit2 a descent in the
-                                       first half (the pass may then stop early); bits 4-5: the two-run path
-                                       was taken and the second run was 1 ascending, 2 descending (reversed
-                                       in place), 3 sorted by the partition tree */
+                                       first half, bit3 one in the second half (with bit1 the pass stops
+                                       early); bits 4-6: the two-run path was taken: bits 4-5 the other run was
+                                       1 ascending, 2 descending (reversed in place), 3 sorted by the partition
+                                       tree; bit 6 the sorted run of at least half the array is the second one */
     int64_t segments;               /* descriptors allocated */
     int64_t status;                 /* 0 or a negative pdq_status */
     int64_t bytes_check;            /* bytes the K4 check kernel read */
@@ -101,8 +102,9 @@ typedef struct pdq_stats {
     int64_t bytes_base;             /* algorithmic bytes of the K7 base-case kernel (not in bytes_algorithmic) */
     int64_t sort_ns;                /* device-timer span of the persistent sorter (first CTA start -> last end) */
     int64_t base_ns;                /*   ... of the base-case kernel (0 if it did not run) */
-    int64_t run_split;              /* K4 two-run path: A[0, run_split) was a sorted prefix merged with the
-                                       rest (0: path not taken); the merge's bytes are in bytes_base */
+    int64_t run_split;              /* K4 two-run path: A[0, run_split) and A[run_split, n) were merged, one of
+                                       them a sorted run of at least half the array (0: path not taken); the
+                                       merge's bytes are in bytes_base */
 } pdq_stats;
 
 /* Fill `cfg` with the reference defaults (driver.py:55-63) and GPU defaults. */

@@ -92,14 +92,17 @@ struct __align__(128) State {
     // and the largest ascent index + 1
     unsigned long long run_d1_inv, run_dl, run_la;
     unsigned long long run_split;  // > 0: A[0, run_split) and A[run_split, n) are merged after the sort
-    unsigned int run_kind;         // the second run was 1 ascending, 2 descending (reversed), 3 sorted by the tree
+    unsigned int run_kind;         // the other run was 1 ascending, 2 descending (reversed), 3 sorted by the tree;
+                                   // + 4 when the sorted run of at least half the array is the second one
     unsigned int pad_e;
     // merge epilogue of the leaf kernel (RunsMerge): progress counters instead of grid barriers, so a CTA
     // only ever waits for work that running CTAs have already claimed
     unsigned long long leaves_done;  // leaves finished (summed per CTA at the end of its leaf loop)
     unsigned long long merge_next;   // next unclaimed merge tile
     unsigned long long merge_done;   // merge tiles written to B
-    unsigned long long pad_d[4];
+    unsigned long long run_fa_inv;   // K4: the smallest ascent index, stored inverted like run_d1_inv
+    unsigned long long rev_begin, rev_end;  // the range the sorter's prologue reverses (K4)
+    unsigned long long pad_d[1];
     // counters (pdq_stats order)
     unsigned long long leaf_count;  // queued base-case segments (K7 kernel input)
     unsigned long long leaf_next;   // K7 kernel claim counter

@@ -1716,16 +1716,17 @@ struct Sorter {
 
 // ---- K4: adjacent-compare reduction with early exit ---------------------------------------------
 // One pass over adjacent pairs: bit 0 a descent was seen, bit 1 an ascent, bit 2 a descent in the first
-// half of the array (or anywhere, for arrays too short for the two-run path).  The pass is cut short
-// once bits 1 and 2 are both set: the input is then neither sorted, nor reversed, nor a sorted prefix of
-// at least half the array followed by a second run.  When it runs to the end, the first and last descent
-// and the last ascent are exact (k_init reads them to recognise two runs: small_sorts.py:76-115's
-// "nearly sorted" case on the GPU is a sorted prefix followed by anything).
+// half of the array, bit 3 a descent in the second half (for arrays too short for the two-run path every
+// descent sets both).  The pass is cut short once bits 1, 2 and 3 are all set: the input is then neither
+// sorted, nor reversed, nor a sorted run of at least half the array next to a second run; uniform input
+// stops after one or two chunks per CTA.  When the pass runs to the end, the first and last descent and the
+// first and last ascent are exact (k_init reads them to recognise two runs: small_sorts.py:76-115's
+// "nearly sorted" case on the GPU is a sorted run of at least half the array next to anything).
 template <class U, bool FLOAT, bool KV>
 __global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Params P) {
     using O = Ord<U, FLOAT>;
     __shared__ unsigned s_pub;
-    __shared__ unsigned long long s_red[3][WARPS];
+    __shared__ unsigned long long s_red[4][WARPS];
     const int tid = threadIdx.x, lane = tid & 31;
     pdl_trigger();  // k_init (one CTA) may be scheduled now; it waits for this grid before reading
     {  // the task ring starts empty (all-ones words match no round tag); k_init pushes after this grid
@@ -1740,12 +1741,24 @@ __global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Param
     const int64_t n = P.n;
     constexpr int E = 4, STEPS = ITEMS / E;  // a thread reads 4 elements (16-byte vectors) per step
     const int64_t CH = (int64_t)THREADS * ITEMS;
-    // a descent at index i < early leaves a sorted prefix shorter than half the array
-    const int64_t early = n >= P.runs_min ? (n + 1) / 2 - 1 : n;
+    // a descent at index i < early leaves a sorted prefix shorter than half the array, one at i >= late a
+    // sorted suffix shorter than half
+    const bool two_run = n >= P.runs_min;
+    const int64_t early = two_run ? (n + 1) / 2 - 1 : n, late = two_run ? n / 2 : 0;
     constexpr unsigned long long NONE = ~0ull;
-    unsigned long long d1 = NONE, dl = 0, la = 0;  // this thread's first descent, last descent + 1, last ascent + 1
+    // this thread's first descent, last descent + 1, first ascent, last ascent + 1
+    unsigned long long d1 = NONE, dl = 0, fa = NONE, la = 0;
     unsigned long long bytes = 0;
-    for (int64_t c0 = (int64_t)blockIdx.x * CH; c0 < n - 1; c0 += (int64_t)gridDim.x * CH) {
+    // Half of the CTAs stride over the chunks of the first half of the array, the others over the second
+    // half: two contiguous windows move through the array (a CTA-contiguous split costs 30 % of the pass's
+    // bandwidth), a thread's indices only grow, and the first wave already sees both halves.
+    const int64_t nchunks = (n - 1 + CH - 1) / CH;
+    const int64_t G = gridDim.x, G1 = G >= 2 ? G / 2 : G, mid = G >= 2 ? nchunks / 2 : nchunks;
+    const bool lower = (int64_t)blockIdx.x < G1;
+    const int64_t ch0 = lower ? (int64_t)blockIdx.x : mid + ((int64_t)blockIdx.x - G1);
+    const int64_t c_end = lower ? mid : nchunks, c_step = lower ? G1 : G - G1;
+    for (int64_t ch = ch0; ch < c_end; ch += c_step) {
+        const int64_t c0 = ch * CH;
         // the verdict so far (its latency overlaps the chunk's loads; threads may leave one chunk apart)
         const unsigned flag = ld_volatile_u32(&P.st->check_bits);
         unsigned bits = 0;
@@ -1793,12 +1806,13 @@ __global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Param
                 if (i + q < n - 1) {
                     const uint64_t x = (uint64_t)O::to(k[q]), y = (uint64_t)O::to(k[q + 1]);
                     if (pless<KV>(y, v[q + 1], x, v[q])) {  // (a thread's indices only grow)
-                        bits |= i + q < early ? 5u : 1u;
+                        bits |= 1u | (i + q < early ? 4u : 0u) | (i + q >= late ? 8u : 0u);
                         if (d1 == NONE) d1 = (unsigned long long)(i + q);
                         dl = (unsigned long long)(i + q) + 1;
                     }
                     if (pless<KV>(x, v[q], y, v[q + 1])) {
                         bits |= 2u;
+                        if (fa == NONE) fa = (unsigned long long)(i + q);
                         la = (unsigned long long)(i + q) + 1;
                     }
                 }
@@ -1815,21 +1829,23 @@ __global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Param
             const int64_t hi = c0 + CH < n ? c0 + CH : n;
             bytes += (unsigned long long)(hi - c0) * (sizeof(U) + (KV ? 4 : 0));
         }
-        if ((flag & 6u) == 6u) break;
+        if ((flag & 14u) == 14u) break;
     }
     // CTA reduction of the run marks, one atomic each
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long a1 = __shfl_xor_sync(0xffffffffu, d1, o), a2 = __shfl_xor_sync(0xffffffffu, dl, o),
-                                 a3 = __shfl_xor_sync(0xffffffffu, la, o);
+                                 a3 = __shfl_xor_sync(0xffffffffu, la, o), a4 = __shfl_xor_sync(0xffffffffu, fa, o);
         d1 = a1 < d1 ? a1 : d1;
         dl = a2 > dl ? a2 : dl;
         la = a3 > la ? a3 : la;
+        fa = a4 < fa ? a4 : fa;
     }
     if (lane == 0) {
         s_red[0][tid >> 5] = d1;
         s_red[1][tid >> 5] = dl;
         s_red[2][tid >> 5] = la;
+        s_red[3][tid >> 5] = fa;
     }
     __syncthreads();
     if (tid == 0) {
@@ -1837,10 +1853,12 @@ __global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Param
             d1 = s_red[0][w] < d1 ? s_red[0][w] : d1;
             dl = s_red[1][w] > dl ? s_red[1][w] : dl;
             la = s_red[2][w] > la ? s_red[2][w] : la;
+            fa = s_red[3][w] < fa ? s_red[3][w] : fa;
         }
         if (d1 != NONE) atomicMax(&P.st->run_d1_inv, ~d1);
         if (dl) atomicMax(&P.st->run_dl, dl);
         if (la) atomicMax(&P.st->run_la, la);
+        if (fa != NONE) atomicMax(&P.st->run_fa_inv, ~fa);
         if (bytes) atomicAdd(&P.st->c_bytes_check, bytes);
     }
 }
@@ -1849,59 +1867,78 @@ __global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Param
 // K4 verdicts: no descent -> sorted; no ascent -> reversed in place; no descent in the first half (the
 // pass then ran to the end) -> two runs: A[0, s) is sorted, s = first descent + 1 >= n / 2, and the rest
 // is left as it is (ascending: a single descent), reversed (no ascent beyond s) or sorted by the tree as
-// the root segment [s, n); the leaf kernel then merges the two runs (RunsMerge).  Anything else: the
-// root segment is the whole array.
+// the root segment [s, n); mirrored, no descent in the second half -> A[s, n) is sorted, s = last descent
+// + 1 <= n / 2, and A[0, s) is left, reversed or sorted by the tree.  The leaf kernel then merges the two
+// runs (RunsMerge).  Anything else: the root segment is the whole array.
 template <class U, bool FLOAT, bool KV>
 __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params P) {
     using S = Sorter<U, FLOAT, KV>;
     Shared &sh = g_sh;
     __shared__ int s_action;
-    __shared__ long long s_root;
+    __shared__ long long s_rb, s_re;
     const int tid = threadIdx.x;
     pdl_wait();     // k_check's verdict
     pdl_trigger();  // the sorter's CTAs may be scheduled; they wait for this grid before reading
     if (tid == 0) {
         S::zero_counters();
-        const unsigned bits = P.st->check_bits;
-        int action = 0;  // 0 = sort, 1 = done (sorted), 2 = reverse
-        long long root = 0;
+        State *st = P.st;
+        const unsigned bits = st->check_bits;
+        int action = 0;  // 0 = sort [rb, re), 1 = done (sorted), 2 = reverse [rb, re)
+        long long rb = 0, re = P.n;
         if (P.n <= 1) action = 1;
         else if (P.use_check && !(bits & 1u)) action = 1;
         else if (P.use_check && !(bits & 2u)) action = 2;
-        else if (P.use_check && !(bits & 4u) && P.n >= P.runs_min) {
-            const unsigned long long s = ~P.st->run_d1_inv + 1;  // the second run starts here
-            P.st->run_split = s;
-            if (P.st->run_dl == s) {  // a single descent: the second run is ascending
-                P.st->run_kind = 1;
+        else if (P.use_check && P.n >= P.runs_min && !(bits & 4u)) {
+            const unsigned long long s = ~st->run_d1_inv + 1;  // the second run starts here
+            st->run_split = s;
+            rb = (long long)s;
+            if (st->run_dl == s) {  // a single descent: the second run is ascending
+                st->run_kind = 1;
                 action = 1;
-            } else if (P.st->run_la <= s) {  // no ascent beyond s: the second run is reversed in place
-                P.st->run_kind = 2;
+            } else if (st->run_la <= s) {  // no ascent beyond s: the second run is reversed in place
+                st->run_kind = 2;
                 action = 2;
             } else {  // the tree sorts [s, n)
-                P.st->run_kind = 3;
-                root = (long long)s;
-                P.st->keys_final = s;
+                st->run_kind = 3;
+            }
+        } else if (P.use_check && P.n >= P.runs_min && !(bits & 8u)) {
+            const unsigned long long s = st->run_dl;  // the sorted second run starts here (last descent + 1)
+            st->run_split = s;
+            re = (long long)s;
+            if (~st->run_d1_inv + 1 == s) {  // a single descent: the first run is ascending (and shorter)
+                st->run_kind = 5;
+                action = 1;
+            } else if (st->run_fa_inv == 0 || ~st->run_fa_inv + 1 >= s) {  // no ascent inside [0, s): reversed
+                st->run_kind = 6;
+                action = 2;
+            } else {  // the tree sorts [0, s)
+                st->run_kind = 7;
             }
         }
         s_action = action;
-        s_root = root;
+        s_rb = rb;
+        s_re = re;
         if (action == 1) {
-            P.st->keys_final = P.n;
-            P.st->done = 1;
+            st->keys_final = P.n;
+            st->done = 1;
         } else if (action == 2) {
-            P.st->reverse = 1;
-            P.st->keys_final = P.n;
-            P.st->done = 1;
-            sh.s_bytes += 2ull * (sizeof(U) + (KV ? 4 : 0)) * (unsigned long long)(P.n - (int64_t)P.st->run_split);
+            st->reverse = 1;
+            st->rev_begin = (unsigned long long)rb;
+            st->rev_end = (unsigned long long)re;
+            st->keys_final = P.n;
+            st->done = 1;
+            sh.s_bytes += 2ull * (sizeof(U) + (KV ? 4 : 0)) * (unsigned long long)(re - rb);
+        } else {
+            st->keys_final = (unsigned long long)(P.n - (re - rb));  // the sorted run is final for the tree
         }
     }
     __syncthreads();
     if (s_action == 0) {
-        const int64_t m = P.n - s_root;
+        const int64_t m = s_re - s_rb;
         int budget = P.budget0;
         if (budget < 0) budget = 63 - __clzll((long long)m);  // driver.py:263: n.bit_length() - 1
         typename S::Bnd none{};
-        S::spawn(P, s_root, P.n, false, none, budget, 0, false, -1);
+        S::spawn(P, s_rb, s_re, false, none, budget, 0, false, -1);
     }
     __syncthreads();
     if (tid == 0) S::flush_counters(P);
@@ -3326,13 +3363,13 @@ __global__ void __launch_bounds__(THREADS, sort_min_blocks<U, KV>()) k_sort(cons
     pdl_wait();  // k_init's root segment and verdict
     if (tid == 0) atomicMax(&P.st->t_sort_b_inv, ~globaltimer_ns());
 
-    // K4 reverse: a non-increasing input (or second run, [run_split, n)) is reversed in place (one read +
-    // one write pass)
+    // K4 reverse: a non-increasing input (or the non-increasing one of two runs), [rev_begin, rev_end), is
+    // reversed in place (one read + one write pass)
     if (ld_volatile_u32(&P.st->reverse)) {
-        const int64_t r0 = (int64_t)P.st->run_split;
+        const int64_t r0 = (int64_t)P.st->rev_begin;
         U *a = (U *)P.a_keys + r0;
         uint32_t *av = KV ? P.a_vals + r0 : nullptr;
-        const int64_t n = P.n - r0, half = n / 2;
+        const int64_t n = (int64_t)P.st->rev_end - r0, half = n / 2;
         const int64_t gt = (int64_t)blockIdx.x * THREADS + tid, gs = (int64_t)gridDim.x * THREADS;
         int64_t done = 0;
         if (n % S::AL == 0 && r0 % S::AL == 0) {

@@ -50,8 +50,8 @@ class SortConfig:
     ``use_break_patterns`` gates the sample perturbation after a bad
     partition, and ``use_partial_insertion`` gates the sortedness check (K4):
     sorted input returns after one pass, reversed input after a reversal, and a
-    sorted prefix of at least half the array (``n >= two_run_min``) is merged
-    with the separately handled rest.
+    sorted prefix or suffix of at least half the array (``n >= two_run_min``)
+    is merged with the separately handled rest.
     """
 
     insertion_threshold: int = 24

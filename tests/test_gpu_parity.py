@@ -255,18 +255,20 @@ def test_sorted_and_reversed_are_one_pass():
     assert same_bytes(got, asc) and st["partition_right_calls"] == 0 and st["check_result"] & 3 == 1
 
 
-def _two_runs(rng, n, s, kind, dtype):
-    """sorted prefix of s elements, then an ascending (1), descending (2) or random (3) rest"""
+def _two_runs(rng, n, s, kind, dtype, mirror=False):
+    """sorted prefix of s elements, then an ascending (1), descending (2) or random (3) rest; mirrored: the
+    sorted run is the suffix [s, n) and the rest comes first"""
     if np.dtype(dtype).kind == "f":
         x = rng.standard_normal(n).astype(dtype)
     else:
         info = np.iinfo(dtype)
         x = rng.integers(info.min, info.max, n, dtype=dtype, endpoint=True)
-    x[:s].sort()
+    big, small = (slice(s, n), slice(0, s)) if mirror else (slice(0, s), slice(s, n))
+    x[big] = np.sort(x[big])
     if kind == 1:
-        x[s:].sort()
+        x[small] = np.sort(x[small])
     elif kind == 2:
-        x[s:] = np.sort(x[s:])[::-1]
+        x[small] = np.sort(x[small])[::-1]
     return x
 
 
@@ -290,6 +292,14 @@ def test_two_run_path_vs_oracle(dtype):
                     assert same_bytes(gv, wv), (n, s, kind)
                 # (a random rest may by chance extend the prefix or be monotone: only the path is asserted)
                 assert st["run_split"] >= s or st["check_result"] & 3 != 3, (n, s, kind, st)
+                # mirrored: the sorted run of at least half the array is the suffix [n - s, n)
+                keys = _two_runs(rng, n, n - s, kind, kd, mirror=True)
+                got, gv, st = gpu_sort(keys, vals, cfg)
+                want, wv = oracle_sort(keys, vals)
+                assert same_bytes(got, want), (n, s, kind, "mirror")
+                if vals is not None:
+                    assert same_bytes(gv, wv), (n, s, kind, "mirror")
+                assert st["run_split"] > 0 or st["check_result"] & 3 != 3, (n, s, kind, st)
 
 
 def test_two_run_path_duplicates_and_kinds():
@@ -315,6 +325,12 @@ def test_two_run_path_duplicates_and_kinds():
     assert same_bytes(got, np.sort(keys)) and (st["check_result"] >> 4) == 2 and st["partition_right_calls"] == 0
     got, _, st = gpu_sort(keys, None, SortConfig(two_run_min=n + 1))
     assert same_bytes(got, np.sort(keys)) and st["run_split"] == 0 and st["partition_right_calls"] >= 1
+    # the mirrored kinds: a short descending / ascending / random first run before a sorted second run
+    for kind, code in ((1, 5), (2, 6), (3, 7)):
+        keys = _two_runs(rng, n, n - s, kind, np.int32, mirror=True)
+        got, _, st = gpu_sort(keys, None, cfg)
+        assert same_bytes(got, np.sort(keys)) and (st["check_result"] >> 4) == code and st["run_split"] == n - s, st
+        assert (st["partition_right_calls"] == 0) == (kind != 3)
     # use_partial_insertion=False switches K4 off altogether (driver.py:63)
     got, _, st = gpu_sort(keys, None, SortConfig(two_run_min=64, use_partial_insertion=False))
     assert same_bytes(got, np.sort(keys)) and st["run_split"] == 0

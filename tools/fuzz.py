@@ -52,6 +52,15 @@ def keys_of(n, dt, pattern):
             x[s:].sort()
         elif kind == 1:
             x[s:] = np.sort(x[s:])[::-1]
+    elif pattern == "suffix":  # anything, then a sorted suffix from a random position
+        s = int(rng.integers(0, n + 1))
+        x = base.copy()
+        x[s:].sort()
+        kind = rng.integers(0, 3)
+        if kind == 0:
+            x[:s].sort()
+        elif kind == 1:
+            x[:s] = np.sort(x[:s])[::-1]
     elif pattern == "nearly":
         x = np.sort(base)
         m = max(1, n // 100)
@@ -79,7 +88,7 @@ while time.time() - t0 < budget:
         n = int(rng.choice([0, 1, 2, 63, 64, 65, 4096, 8188, 8189, 24572, 24573]))
     dt = DT[rng.integers(0, 4)]
     kv = rng.random() < 0.35
-    pattern = str(rng.choice(["uniform", "few", "sorted", "reversed", "runs", "prefix", "nearly", "saw", "organ", "special"]))
+    pattern = str(rng.choice(["uniform", "few", "sorted", "reversed", "runs", "prefix", "suffix", "nearly", "saw", "organ", "special"]))
     cfg = SortConfig(use_partition_left=bool(rng.random() < 0.85), use_break_patterns=bool(rng.random() < 0.85),
                      use_partial_insertion=bool(rng.random() < 0.85),
                      bad_partition_shift=int(rng.choice([1, 2, 3, 3, 3, 5])),
@@ -104,7 +113,7 @@ while time.time() - t0 < budget:
     else:
         o = np.lexsort((vals, keys))
         ok = np.array_equal(got, keys[o]) and np.array_equal(vd.cpu().numpy().view(np.uint32), vals[o])
-    key = (pattern, "kv" if kv else "k", (st["check_result"] >> 4) & 3)
+    key = (pattern, "kv" if kv else "k", (st["check_result"] >> 4) & 7)
     hist[key] = hist.get(key, 0) + 1
     if not ok or st["status"] != 0:
         np.save(f"gpurun_out/fuzz_fail_{seed}_{it}_keys.npy", keys)

@@ -26,7 +26,7 @@ def check(name, keys, vals=None, cfg=None, want_kind=None):
     else:
         order = np.lexsort((vals, keys))
         ok = np.array_equal(got, keys[order]) and np.array_equal(vd.cpu().numpy().view(np.uint32), vals[order])
-    kind = (st["check_result"] >> 4) & 3
+    kind = (st["check_result"] >> 4) & 7
     if not ok or (want_kind is not None and kind != want_kind):
         bad += 1
         print("FAIL", name, "ok", ok, "kind", kind, "want", want_kind, "split", st["run_split"], flush=True)
@@ -59,6 +59,14 @@ for dtype in dtypes:
             for kind in (1, 2, 3):
                 x = runs(n, s, kind, dtype)
                 check(f"{np.dtype(dtype).name} n={n} s={s} kind={kind}", x, cfg=cfg_small)
+                # mirrored: sorted suffix of s elements after an ascending / descending / random first run
+                y = runs(n, s, 3, dtype)[::-1].copy()  # descending suffix ...
+                y[n - s:] = np.sort(y[n - s:])         # ... made ascending
+                if kind == 1:
+                    y[: n - s].sort()
+                elif kind == 2:
+                    y[: n - s] = np.sort(y[: n - s])[::-1]
+                check(f"{np.dtype(dtype).name} n={n} s={s} kind={kind} mirror", y, cfg=cfg_small)
                 if not only_i32 and n <= (1 << 18):
                     v = rng.permutation(n).astype(np.uint32)
                     check(f"{np.dtype(dtype).name}+kv n={n} s={s} kind={kind}", x, v, cfg=cfg_small)
