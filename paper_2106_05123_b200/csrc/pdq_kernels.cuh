@@ -1801,21 +1801,33 @@ __global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Param
                 k[E] = a[i + E];
                 if constexpr (KV) v[E] = P.a_vals[i + E];
             }
+            // ordered images once per element; the four pairs' verdicts as two 4-bit masks, so the 64-bit
+            // index bookkeeping runs once per vector (and only when a mask is non-zero)
+            uint64_t o[E + 1];
+#pragma unroll
+            for (int q = 0; q <= E; ++q) o[q] = (uint64_t)O::to(k[q]);
+            unsigned dm = 0, am = 0;
 #pragma unroll
             for (int q = 0; q < E; ++q) {
-                if (i + q < n - 1) {
-                    const uint64_t x = (uint64_t)O::to(k[q]), y = (uint64_t)O::to(k[q + 1]);
-                    if (pless<KV>(y, v[q + 1], x, v[q])) {  // (a thread's indices only grow)
-                        bits |= 1u | (i + q < early ? 4u : 0u) | (i + q >= late ? 8u : 0u);
-                        if (d1 == NONE) d1 = (unsigned long long)(i + q);
-                        dl = (unsigned long long)(i + q) + 1;
-                    }
-                    if (pless<KV>(x, v[q], y, v[q + 1])) {
-                        bits |= 2u;
-                        if (fa == NONE) fa = (unsigned long long)(i + q);
-                        la = (unsigned long long)(i + q) + 1;
-                    }
-                }
+                dm |= (pless<KV>(o[q + 1], v[q + 1], o[q], v[q]) ? 1u : 0u) << q;
+                am |= (pless<KV>(o[q], v[q], o[q + 1], v[q + 1]) ? 1u : 0u) << q;
+            }
+            if (i + E > n - 1) {  // the array's last vectors: pairs (j, j + 1) exist for j < n - 1
+                const int64_t left = n - 1 - i;
+                const unsigned keep = left <= 0 ? 0u : (1u << left) - 1u;
+                dm &= keep;
+                am &= keep;
+            }
+            if (dm) {  // (a thread's indices only grow)
+                const int64_t lo = i + (__ffs(dm) - 1), hi = i + (31 - __clz(dm));
+                bits |= 1u | (lo < early ? 4u : 0u) | (hi >= late ? 8u : 0u);
+                if (d1 == NONE) d1 = (unsigned long long)lo;
+                dl = (unsigned long long)hi + 1;
+            }
+            if (am) {
+                bits |= 2u;
+                if (fa == NONE) fa = (unsigned long long)(i + (__ffs(am) - 1));
+                la = (unsigned long long)(i + (31 - __clz(am))) + 1;
             }
         }
         bits = __reduce_or_sync(0xffffffffu, bits);
