@@ -1722,8 +1722,11 @@ struct Sorter {
 // stops after one or two chunks per CTA.  When the pass runs to the end, the first and last descent and the
 // first and last ascent are exact (k_init reads them to recognise two runs: small_sorts.py:76-115's
 // "nearly sorted" case on the GPU is a sorted run of at least half the array next to anything).
+#ifndef PDQ_CHECK_MINB
+#define PDQ_CHECK_MINB 1
+#endif
 template <class U, bool FLOAT, bool KV>
-__global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(THREADS, PDQ_CHECK_MINB) k_check(const __grid_constant__ Params P) {
     using O = Ord<U, FLOAT>;
     __shared__ unsigned s_pub;
     __shared__ unsigned long long s_red[4][WARPS];
@@ -1739,8 +1742,11 @@ __global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Param
     __syncthreads();
     const U *a = (const U *)P.a_keys;
     const int64_t n = P.n;
-    constexpr int E = 4, STEPS = ITEMS / E;  // a thread reads 4 elements (16-byte vectors) per step
-    const int64_t CH = (int64_t)THREADS * ITEMS;
+#ifndef PDQ_CHECK_STEPS
+#define PDQ_CHECK_STEPS 4
+#endif
+    constexpr int E = 4, STEPS = PDQ_CHECK_STEPS;  // a thread reads 4 elements (16-byte vectors) per step
+    const int64_t CH = (int64_t)THREADS * STEPS * E;
     // a descent at index i < early leaves a sorted prefix shorter than half the array, one at i >= late a
     // sorted suffix shorter than half
     const bool two_run = n >= P.runs_min;
@@ -1762,44 +1768,67 @@ __global__ void __launch_bounds__(THREADS) k_check(const __grid_constant__ Param
         // the verdict so far (its latency overlaps the chunk's loads; threads may leave one chunk apart)
         const unsigned flag = ld_volatile_u32(&P.st->check_bits);
         unsigned bits = 0;
+        // all of the chunk's loads first (a whole chunk needs no bounds checks: one 16-byte vector per
+        // step and thread in flight, the element after each vector from the next lane or, for lane 31,
+        // by one scalar load); the array's last chunk loads element by element
+        U kk[STEPS][E + 1];
+        uint32_t vv[STEPS][E + 1];
+        const bool whole = c0 + CH < n;
+        if (whole) {
 #pragma unroll
-        for (int st = 0; st < STEPS; ++st) {
-            const int64_t i = c0 + ((int64_t)st * THREADS + tid) * E;
-            U k[E + 1];
-            uint32_t v[E + 1];
-#pragma unroll
-            for (int q = 0; q <= E; ++q) {
-                k[q] = 0;
-                v[q] = 0;
-            }
-            if (i + E <= n) {
+            for (int st = 0; st < STEPS; ++st) {
+                const int64_t i = c0 + ((int64_t)st * THREADS + tid) * E;
                 if constexpr (sizeof(U) == 4) {
                     const uint4 y = __ldg(reinterpret_cast<const uint4 *>(a + i));
-                    k[0] = (U)y.x; k[1] = (U)y.y; k[2] = (U)y.z; k[3] = (U)y.w;
+                    kk[st][0] = (U)y.x; kk[st][1] = (U)y.y; kk[st][2] = (U)y.z; kk[st][3] = (U)y.w;
                 } else {
                     const ulonglong2 y0 = __ldg(reinterpret_cast<const ulonglong2 *>(a + i));
                     const ulonglong2 y1 = __ldg(reinterpret_cast<const ulonglong2 *>(a + i + 2));
-                    k[0] = (U)y0.x; k[1] = (U)y0.y; k[2] = (U)y1.x; k[3] = (U)y1.y;
+                    kk[st][0] = (U)y0.x; kk[st][1] = (U)y0.y; kk[st][2] = (U)y1.x; kk[st][3] = (U)y1.y;
                 }
                 if constexpr (KV) {
                     const uint4 z = __ldg(reinterpret_cast<const uint4 *>(P.a_vals + i));
-                    v[0] = z.x; v[1] = z.y; v[2] = z.z; v[3] = z.w;
+                    vv[st][0] = z.x; vv[st][1] = z.y; vv[st][2] = z.z; vv[st][3] = z.w;
+                } else {
+                    vv[st][0] = vv[st][1] = vv[st][2] = vv[st][3] = 0;
                 }
-            } else {
-#pragma unroll
-                for (int q = 0; q < E; ++q)
-                    if (i + q < n) {
-                        k[q] = a[i + q];
-                        if constexpr (KV) v[q] = P.a_vals[i + q];
-                    }
+                kk[st][E] = 0;
+                vv[st][E] = 0;
+                if (lane == 31) {
+                    kk[st][E] = __ldg(a + i + E);
+                    if constexpr (KV) vv[st][E] = __ldg(P.a_vals + i + E);
+                }
             }
-            // the element after this thread's vector: the next lane's first (lane 31 loads it)
-            if constexpr (sizeof(U) == 4) k[E] = (U)__shfl_down_sync(0xffffffffu, (uint32_t)k[0], 1);
-            else k[E] = (U)__shfl_down_sync(0xffffffffu, (unsigned long long)k[0], 1);
-            if constexpr (KV) v[E] = __shfl_down_sync(0xffffffffu, v[0], 1);
-            if (lane == 31 && i + E < n) {
-                k[E] = a[i + E];
-                if constexpr (KV) v[E] = P.a_vals[i + E];
+        } else {
+#pragma unroll
+            for (int st = 0; st < STEPS; ++st) {
+                const int64_t i = c0 + ((int64_t)st * THREADS + tid) * E;
+#pragma unroll
+                for (int q = 0; q <= E; ++q) {
+                    kk[st][q] = 0;
+                    vv[st][q] = 0;
+                    if (i + q < n && (q < E || lane == 31)) {
+                        kk[st][q] = a[i + q];
+                        if constexpr (KV) vv[st][q] = P.a_vals[i + q];
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int st = 0; st < STEPS; ++st) {
+            const int64_t i = c0 + ((int64_t)st * THREADS + tid) * E;
+            U(&k)[E + 1] = kk[st];
+            uint32_t(&v)[E + 1] = vv[st];
+            // the element after this thread's vector: the next lane's first (lane 31 loaded it)
+            {
+                U nk;
+                if constexpr (sizeof(U) == 4) nk = (U)__shfl_down_sync(0xffffffffu, (uint32_t)k[0], 1);
+                else nk = (U)__shfl_down_sync(0xffffffffu, (unsigned long long)k[0], 1);
+                const uint32_t nv = KV ? __shfl_down_sync(0xffffffffu, v[0], 1) : 0u;
+                if (lane != 31) {
+                    k[E] = nk;
+                    v[E] = nv;
+                }
             }
             // ordered images once per element; the four pairs' verdicts as two 4-bit masks, so the 64-bit
             // index bookkeeping runs once per vector (and only when a mask is non-zero)
