@@ -24,7 +24,7 @@ int pdq::set_err(int code, const char *fmt, const char *detail) {
 }
 
 extern "C" const char *pdq_last_error(void) { return g_err; }
-extern "C" const char *pdq_version(void) { return "pdq_b200 0.1.0 (sm_100a)"; }
+extern "C" const char *pdq_version(void) { return "pdq_b200 0.2.0 (sm_100a)"; }
 
 extern "C" void pdq_config_default(pdq_config *c) {
     memset(c, 0, sizeof(*c));

@@ -2279,9 +2279,10 @@ struct BigLeaf {
     // Each element only moves inside its bucket; a bucket of <= 13 keys lies in one aligned or one offset
     // window, so after the two passes every bucket -- and so the leaf -- is in order.  Slots q < a0 read
     // as 0 (below every key), q >= qend as ~0 (above every key); neither is ever stored.
-    __device__ __forceinline__ static void window_sort(uint32_t *kc, uint32_t a0, uint32_t qend, U *dst) {
+    // `sorted`: the bucketed leaf is already in order (every bucket holds one distinct key): copy-out only
+    __device__ __forceinline__ static void window_sort(uint32_t *kc, uint32_t a0, uint32_t qend, U *dst, bool sorted) {
         const uint32_t t = threadIdx.x;
-        if (WIN * t < qend) {
+        if (!sorted && WIN * t < qend) {
             U w[WIN];
 #pragma unroll
             for (int j = 0; j < 6; ++j) ld_chunk(kc + swz_chunk(t, j), w + 4 * j);
@@ -2296,8 +2297,8 @@ struct BigLeaf {
 #pragma unroll
             for (int j = 0; j < 6; ++j) st_chunk(kc + swz_chunk(t, j), w + 4 * j);
         }
-        bsync();
-        if (WIN * t + HALF < qend) {
+        if (!sorted) bsync();
+        if (!sorted && WIN * t + HALF < qend) {
             U w[WIN];
             const bool second = WIN * (t + 1) < qend;
 #pragma unroll
@@ -2513,7 +2514,11 @@ struct BigLeaf {
             bsync();
             PHASE_MARK(1);
             const uint32_t a0 = (uint32_t)(b & 3);
-            const bool fast = PDQ_BIG_SKIP || cmax <= FAST_CMAX;
+            // A leaf spanning fewer than BBK / 2 distinct key values has at most one value per bucket (the
+            // map advances by more than one bucket per key step), so bucketing alone sorts it: float32 keys
+            // at 2^26+ (2^23 values per binade), low-cardinality integers
+            const bool exact = range < (U)(BBK / 2);
+            const bool fast = PDQ_BIG_SKIP || exact || cmax <= FAST_CMAX;
 #pragma unroll
             for (int jv = 0; jv < BI / 4; ++jv) {
                 if (jv < nvec) {
@@ -2534,7 +2539,7 @@ struct BigLeaf {
             bsync();
             PHASE_MARK(2);
             if (fast) {
-                window_sort(kc, a0, a0 + (uint32_t)m, (U *)P.a_keys + b);
+                window_sort(kc, a0, a0 + (uint32_t)m, (U *)P.a_keys + b, exact);
                 if (tid == 0) {
                     sh.s_base++;
                     sh.s_bytes += 8ull * m;
