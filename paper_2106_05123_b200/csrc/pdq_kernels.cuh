@@ -1759,9 +1759,12 @@ __global__ void __launch_bounds__(THREADS, PDQ_CHECK_MINB) k_check(const __grid_
     // half: two contiguous windows move through the array (a CTA-contiguous split costs 30 % of the pass's
     // bandwidth), a thread's indices only grow, and the first wave already sees both halves.
     const int64_t nchunks = (n - 1 + CH - 1) / CH;
-    const int64_t G = gridDim.x, G1 = G >= 2 ? G / 2 : G, mid = G >= 2 ? nchunks / 2 : nchunks;
-    const bool lower = (int64_t)blockIdx.x < G1;
-    const int64_t ch0 = lower ? (int64_t)blockIdx.x : mid + ((int64_t)blockIdx.x - G1);
+    // (Even CTAs take the first half, odd CTAs the second: whatever subset of the grid is resident sees both
+    // halves -- with the halves split by CTA index, a grid of two waves ran the whole first half before any
+    // CTA of the second half started.)
+    const int64_t G = gridDim.x, G1 = G >= 2 ? (G + 1) / 2 : G, mid = G >= 2 ? nchunks / 2 : nchunks;
+    const bool lower = G < 2 || (blockIdx.x & 1u) == 0;
+    const int64_t ch0 = lower ? (int64_t)(blockIdx.x >> (G >= 2 ? 1 : 0)) : mid + (int64_t)(blockIdx.x >> 1);
     const int64_t c_end = lower ? mid : nchunks, c_step = lower ? G1 : G - G1;
     for (int64_t ch = ch0; ch < c_end; ch += c_step) {
         const int64_t c0 = ch * CH;
