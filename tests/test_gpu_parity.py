@@ -366,6 +366,19 @@ def test_two_run_patterns_beat_uniform():
     assert ms["C2.asc_tail"] < 0.7 * ms["uniform"] and ms["C2.organ"] < 0.7 * ms["uniform"], ms
 
 
+def test_check_pass_stops_early_on_uniform_input():
+    # K4 must cost uniform input almost nothing: the pass stops once an ascent and descents in both halves
+    # have been seen (a two-wave grid once scanned the whole first half before stopping: 42 % of 2^28 keys)
+    n = 1 << 26
+    g = torch.Generator(device=DEV)
+    g.manual_seed(8)
+    kd = torch.randint(-(2**31), 2**31, (n,), dtype=torch.int64, device=DEV, generator=g).to(torch.int32)
+    st = sort_device(kd)
+    assert bool((kd[1:] >= kd[:-1]).all().item())
+    assert st["check_result"] & 15 == 15 and st["run_split"] == 0
+    assert st["bytes_check"] <= 4 * n // 4, st["bytes_check"]
+
+
 def test_extreme_values_and_zeros():
     for dt in (np.int32, np.int64):
         info = np.iinfo(dt)
