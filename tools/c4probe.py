@@ -2,7 +2,7 @@
   python tools/c4probe.py"""
 import sys
 import numpy as np, torch
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, __file__.rsplit('/tools/', 1)[0])
 from paper_2106_05123_b200 import DeviceSorter, workloads
 n = 1 << 26
 cases = {"C4.normal": workloads.c4("normal", n), "uniform f32": np.random.default_rng(1).random(n, dtype=np.float32),

@@ -1,5 +1,7 @@
+"""Bytes the K4 check pass reads before it stops on uniform keys, and the prologue time, 2^20 .. 2^28:
+  python tools/ckprobe.py"""
 import sys, torch
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, __file__.rsplit('/tools/', 1)[0])
 from paper_2106_05123_b200 import DeviceSorter
 g = torch.Generator(device="cuda"); g.manual_seed(1)
 for lg in (20, 22, 24, 26, 28):
