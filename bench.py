@@ -509,6 +509,14 @@ def run_ours(args, rank, world, local_rank):
                 "bytes_algorithmic_per_launch": kstats["bytes_base"], "kernel_ms": lf_ms,
                 "kernel_share_of_step": lf_ms / step_avg,
             },
+            "roofline_check": {
+                "bound": "hbm", "kernel": "k_check (K4 adjacent-compare pass; the span also holds the state memset "
+                                          "and k_init, ~20 us)",
+                "achieved": kstats["bytes_check"] / (statistics.mean(pro_ms) / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": kstats["bytes_check"] / (statistics.mean(pro_ms) / 1e3) / 1e9 / peak,
+                "bytes_algorithmic_per_launch": kstats["bytes_check"], "kernel_ms": statistics.mean(pro_ms),
+                "check_result": kstats["check_result"], "run_split": kstats["run_split"],
+            },
             "phase_ms": {"prologue": statistics.mean(pro_ms), "k_sort": ks_ms, "leaf": lf_ms,
                          "how": "CUDA events around each kernel in a separate kernel-timing pass of "
                                 f"{KT} sorts (events between kernels disable their programmatic overlap)",
