@@ -104,7 +104,9 @@ Layout layout(int dtype, int has_payload, int64_t n) {
     off += a256(segs * sizeof(Seg));
     // outstanding tasks <= tiles of live (disjoint) segments + claimed-but-unprocessed
     uint64_t q = (uint64_t)n / (TILE / 2) + 2 * ((uint64_t)n / MIN_BASE) + 2 * segs + 16384;  // tiles >= TILE/2
-    int lq = 14;
+    // at least 2^17 entries (1 MiB): ring positions only grow during a sort, and a degenerate sort of a few
+    // million elements (tiny segments taking many one-tile digit passes) issues tens of thousands of them
+    int lq = 17;
     while ((1ull << lq) < q) ++lq;
     L.log_q = lq;
     L.ring = off;

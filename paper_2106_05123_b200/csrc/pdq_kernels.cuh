@@ -1270,6 +1270,12 @@ struct Sorter {
         csync();
         const int nseq = sh.rl_seq;
         for (int i = 0; i < nseq; ++i) {
+            // This loop can run for a millisecond (up to 256 children started one after another).  The CTA
+            // holds a claimed ring position all that time; if the other CTAs push a whole ring's worth of
+            // tasks meanwhile (many one-tile digit passes of tiny segments), the slot is overwritten before it
+            // is read and its task is lost (found by tools/fuzz.py: the queue stalled).  Copying the task out
+            // of the ring as soon as it appears bounds the exposure to one iteration.
+            if (tid == 0 && sh.nstate == 1) poll_next(P);
             const int d = seq[i];
             const int64_t tb = d ? (int64_t)E[d - 1] : sg.begin, te = (int64_t)E[d];
             if (nrbit >= NBITS) {

@@ -366,6 +366,21 @@ def test_two_run_patterns_beat_uniform():
     assert ms["C2.asc_tail"] < 0.7 * ms["uniform"] and ms["C2.organ"] < 0.7 * ms["uniform"], ms
 
 
+@pytest.mark.parametrize("n,period", [(3356801, 1757), (8000000, 4400)])
+def test_forced_fallback_many_tiny_digit_passes(n, period):
+    # saw-tooth keys with a 2-bit payload under the forced fallback and 1024-element leaves: ~1800+ runs of one
+    # key each take fifteen one-tile digit passes over the payload's zero bits while the CTAs that start the
+    # children of the wide passes are busy for a millisecond -- ring positions wrap past a claimed slot (the
+    # task queue once stalled here: a task overwritten before its claimer read it; tools/fuzz.py seed 29)
+    rng = np.random.default_rng(29)
+    keys = (np.arange(n) % period).astype(np.int32)
+    vals = rng.integers(0, 4, n).astype(np.uint32)
+    got_k, got_v, st = gpu_sort(keys, vals, SortConfig(base_case_size=1024, bad_budget=0))
+    order = np.lexsort((vals, keys))
+    assert same_bytes(got_k, keys[order]) and same_bytes(got_v, vals[order])
+    assert st["status"] == 0 and st["radix_fallbacks"] >= 1
+
+
 def test_check_pass_stops_early_on_uniform_input():
     # K4 must cost uniform input almost nothing: the pass stops once an ascent and descents in both halves
     # have been seen (a two-wave grid once scanned the whole first half before stopping: 42 % of 2^28 keys)

@@ -105,7 +105,14 @@ while time.time() - t0 < budget:
                 keys, vals = keys[o], vals[o]
     kd = torch.from_numpy(keys.copy()).cuda()
     vd = None if vals is None else torch.from_numpy(vals.copy().view(np.int32)).cuda()
-    st = sort_device(kd, vd, cfg)
+    try:
+        st = sort_device(kd, vd, cfg)
+    except Exception as exc:  # a device-side failure: keep the input that caused it
+        np.save(f"gpurun_out/fuzz_exc_{seed}_{it}_keys.npy", keys)
+        if vals is not None:
+            np.save(f"gpurun_out/fuzz_exc_{seed}_{it}_vals.npy", vals)
+        print("EXCEPTION", it, n, np.dtype(dt).name, kv, pattern, cfg, repr(exc), flush=True)
+        sys.exit(2)
     got = kd.cpu().numpy()
     if vals is None:
         want = np.sort(keys, kind="stable")
