@@ -128,6 +128,9 @@ while time.time() - t0 < budget:
             np.save(f"gpurun_out/fuzz_fail_{seed}_{it}_vals.npy", vals)
         print("FAIL", it, n, np.dtype(dt).name, kv, pattern, cfg, st, flush=True)
         sys.exit(1)
-print(f"fuzz ok: {it} sorts in {time.time() - t0:.0f} s (seed {seed})")
 two = sum(v for k, v in hist.items() if k[2])
-print(f"two-run path taken in {two} sorts; by (pattern, kv, kind):", {k: v for k, v in sorted(hist.items()) if k[2]})
+print(f"fuzz ok: {it} sorts in {time.time() - t0:.0f} s (seed {seed}); two-run path taken in {two} sorts", flush=True)
+try:
+    print("by (pattern, kv, kind):", {k: v for k, v in sorted(hist.items()) if k[2]})
+except BrokenPipeError:  # piped into head
+    pass
