@@ -3138,11 +3138,19 @@ struct RunsMerge {
     }
     __device__ __forceinline__ static void bsync() { asm volatile("bar.sync 1, %0;" ::"n"(BT) : "memory"); }
 
-    // thread 0 waits until *counter >= target (bracketed by CTA barriers and gpu-scope fences)
-    __device__ static void wait_for(const unsigned long long *counter, unsigned long long target) {
+    // thread 0 waits until *counter >= target (bracketed by CTA barriers and gpu-scope fences); like the
+    // sorter's ring poll it gives up after 10 s and reports through the status word, never hangs
+    __device__ static void wait_for(const Params &P, const unsigned long long *counter, unsigned long long target) {
         bsync();
         if (threadIdx.x == 0) {
-            while (*(const volatile unsigned long long *)counter < target) __nanosleep(128);
+            const uint64_t t0 = globaltimer_ns();
+            while (*(const volatile unsigned long long *)counter < target) {
+                if (globaltimer_ns() - t0 > WATCHDOG_NS) {
+                    atomicCAS(&P.st->status, 0, -8);
+                    break;
+                }
+                __nanosleep(128);
+            }
             __threadfence();
         }
         bsync();
@@ -3186,7 +3194,7 @@ struct RunsMerge {
             __threadfence();
             bsync();
             if (tid == 0 && sh.s_base) atomicAdd(&P.st->leaves_done, sh.s_base);
-            wait_for(&P.st->leaves_done, total);
+            wait_for(P, &P.st->leaves_done, total);
         }
         // The window that changes: first-run elements <= the second run's smallest stay where they are, and
         // so do second-run elements >= the first run's largest (appending slightly newer keys to a sorted
@@ -3325,7 +3333,7 @@ struct RunsMerge {
             bsync();
             if (tid == 0) atomicAdd(&P.st->merge_done, (unsigned long long)nb);
         }
-        wait_for(&P.st->merge_done, (unsigned long long)ntiles);  // B holds the merged window
+        wait_for(P, &P.st->merge_done, (unsigned long long)ntiles);  // B holds the merged window
         {  // copy the window back, 16-byte vectors (o0 is a multiple of 8 elements)
             constexpr int KPV = 16 / (int)sizeof(U);
             const int64_t gt = (int64_t)blockIdx.x * BT + tid, gs = (int64_t)gridDim.x * BT;
